@@ -1,0 +1,354 @@
+#!/usr/bin/env python3
+"""Benchmark: p-CG-sh iterations/s + achieved HBM GB/s, 3D Poisson 512^3 fp64.
+
+BASELINE.json metric / config 3: 7-point Laplacian on 512^3 (134,217,728 DOF),
+matrix-free, unpreconditioned, b = A * (1/sqrt(n)), x0 = 0, fixed 500 p-CG-sh
+iterations (rtol 0), sigma = 2.30188679245283 (the value the reference's
+selection rule gives at 32^3..128^3).
+
+A "step" is one full solve through the drop-in API (init + 500 fused
+iterations + the reference's true-residual cadence).  `value` is iterations/s
+with b resident in HBM; `e2e` is the same solve called with a pinned HOST
+right-hand side and the solution copied back to host memory, both copies
+inside the timed region.  The inputs (8 x 1 GiB vectors) exceed the 126 MB L2,
+so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU); each rank solves its own
+replica (the z-slab distributed solver is not built yet: "scaling": "weak",
+parallelism "replicas").  `--impl reference` times the CPU oracle (a
+restatement of the reference `kpl` package's single-threaded numpy/numba
+path, oracle/kpl_oracle.py) on the host, one p-CG-sh iteration per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N3 = 512
+ITERS = 500
+SIGMA = 2.30188679245283
+BYTES_PER_DOF = 96            # 6 state vectors read + written once
+METRIC = "p-CG-sh iters/s + achieved HBM GB/s, 3D Poisson 512³ fp64 at 1/2/4/8 B200"
+UNIT = "iterations/s"
+WORKLOAD = ("config3: 3D Poisson 7-point 512^3 matrix-free fp64, M=I, b=A*1/sqrt(n), x0=0, "
+            "500 fixed p-CG-sh iterations, sigma=2.30188679245283")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profiled_traffic():
+    """Per-launch DRAM bytes of the fused iteration kernel from the committed
+    ncu capture (profiles/ncu_pcgsh_iter.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_pcgsh_iter.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200 import _lib, device as Dv
+    from paper_1706_05988_b200.solvers import _Solve
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    A = K.Stencil3D(N3, N3, N3)
+    n = A.n
+    cfg = K.SolverConfig(method="pcg_sh", shift=SIGMA, max_iters=ITERS, rtol=0.0)
+    # b = A * (1/sqrt(n)) computed by the device SpMV (harness.build_rhs, ones_solution)
+    b = K.spmv(A, torch.full((n,), 1.0 / math.sqrt(n), dtype=torch.float64, device=dev))
+    lib = _lib.load()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (also checks the run converges the same way every time)
+    for _ in range(args.warmup):
+        res = K.solve(A, None, b, None, cfg)
+    final_rel = res.history[-1].rnorm_true / math.sqrt(float(torch.dot(b, b)))
+
+    # ---- timed: K solves, inputs resident in HBM
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    l0 = lib.kpl_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        res = K.solve(A, None, b, None, cfg)
+    e1.record()
+    barrier()
+    launches = lib.kpl_launch_count() - l0
+    clk = clocks.stop()
+    t_dev = max_over_ranks(e0.elapsed_time(e1) / 1000.0)
+    iters_done = res.iterations
+    value = world * iters_done * args.steps / t_dev
+
+    # ---- e2e: pinned host b in, host x out, copies inside the timed region
+    b_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    b_host.copy_(b)
+    K.solve(A, None, b_host, None, cfg)
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(args.steps):
+        r2 = K.solve(A, None, b_host, None, cfg)
+        _ = r2.x[0].item()
+    f1.record()
+    barrier()
+    t_e2e = max_over_ranks(f0.elapsed_time(f1) / 1000.0)
+    e2e = world * r2.iterations * args.steps / t_e2e
+    hist_bytes = 48 * (r2.iterations + 1)
+
+    # ---- dominant kernel: the fused p-CG-sh iteration sweep, timed alone
+    S = _Solve(A, None, b, None, K.SolverConfig(method="pcg_sh", shift=SIGMA, max_iters=100, rtol=0.0))
+    S.init()
+    S.iterate(1)                      # j=0 (cadence row 0 + first update)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 9                          # j = 1..9: no cadence kernel, iteration sweeps only
+    k0.record()
+    S.iterate(reps)
+    k1.record()
+    torch.cuda.synchronize()
+    t_kernel = k0.elapsed_time(k1) / 1000.0 / reps
+    alg_bytes = BYTES_PER_DOF * n
+    achieved = alg_bytes / t_kernel / 1e9
+    peak, peak_kind = peaks()
+    traffic = profiled_traffic()
+
+    # whole-solve algorithmic bytes: init (b,x0 reads; r,w writes ~ 40 B/DOF) +
+    # 500 x 96 B/DOF + 50 cadence sweeps x 16 B/DOF
+    solve_bytes = n * (40 + BYTES_PER_DOF * iters_done + 16 * (iters_done // 10 + 1))
+    hbm_gbs = solve_bytes * args.steps / t_dev / 1e9 * world
+
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_dev / args.steps * 1000.0,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (generated operator and rhs; no dataset)",
+        "config": {
+            "workload": WORKLOAD,
+            "n": n,
+            "iterations_per_step": iters_done,
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "l2": "no flush: 8 resident vectors of 1 GiB each >> 126 MB L2",
+            "final_true_rel_residual": final_rel,
+        },
+        "hbm_gbs": hbm_gbs,
+        "hbm_frac_of_measured": hbm_gbs / peak / world,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n + hist_bytes + 128},
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "kernel": "stencil_sweep<2, InVec<0>, BodyPcgIter<0>> (fused SpMV + 9 recurrences + dots)",
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "launch_ms": t_kernel * 1000.0,
+            "peak_kind": peak_kind,
+        },
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.cpu_iters)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------- CPU baseline
+
+def _cpu_setup():
+    import numpy as np
+
+    from oracle import kpl_oracle as O
+    A = O.StencilSpec(N3, N3, N3, 6.0)
+    b = O.spmv(A, np.full(A.n, 1.0 / math.sqrt(A.n)))
+    return O, A, b
+
+
+def cpu_iterations(nsteps, O=None, A=None, b=None, warm=0):
+    """Time `nsteps` p-CG-sh iterations of the oracle on the 512^3 problem
+    (after `warm` untimed ones).  Returns seconds per iteration list."""
+    import numpy as np
+    if O is None:
+        O, A, b = _cpu_setup()
+    times = []
+    marks = []
+
+    def cb(st):
+        marks.append(time.perf_counter())
+
+    total = warm + nsteps
+    O.solve_pcg_shifted(A, None, b, None,
+                        O.Config(method="pcg_sh", shift=SIGMA, max_iters=total, rtol=0.0),
+                        callback=cb)
+    # record k is reached after update k-1; iteration k-1 = marks[k] - marks[k-1]
+    for k in range(warm + 1, total + 1):
+        times.append(marks[k] - marks[k - 1])
+    return times
+
+
+def cpu_baseline(iters):
+    O, A, b = _cpu_setup()
+    times = cpu_iterations(iters, O, A, b, warm=0)
+    per = sum(times) / len(times)
+    return {"value": 1.0 / per, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": (f"{len(times)} p-CG-sh iterations of the 512^3 problem with the CPU "
+                       "oracle (numpy ufuncs + C restatement of the reference's kernels, "
+                       "single thread like the reference); includes its true-residual cadence"),
+            "seconds_per_iteration": per}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    O, A, b = _cpu_setup()
+    steps = args.steps
+    warm = min(args.warmup, 1)
+    times = cpu_iterations(steps, O, A, b, warm=warm)
+    per = sum(times) / len(times)
+    value = 1.0 / per
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": warm, "ms_per_step": per * 1000.0, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated operator and rhs; no dataset)",
+        "config": {"workload": WORKLOAD, "n": A.n, "step": "one p-CG-sh iteration (bounded sample)"},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{steps} iterations of the 512^3 problem, oracle restatement "
+                                   "of the single-threaded reference path"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

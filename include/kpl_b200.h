@@ -1,0 +1,192 @@
+/*
+ * kpl_b200.h -- C ABI of the B200-native shifted pipelined CG (p-CG-sh) path.
+ *
+ * Drop-in boundary for the reference package `kpl` (arXiv 1706.05988 lab).
+ * The reference's "FFI" for this path is its numba layer plus the solver
+ * loop that drives it; each entry point below names the reference interface
+ * it replaces (file:line into pkg/src/kpl/).
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless stated otherwise; sizes are
+ *    element counts; `stream` is a cudaStream_t passed as void*.
+ *  - The library never allocates or frees device memory.  Scratch space is a
+ *    caller buffer of kpl_workspace_bytes() bytes (256-byte aligned).
+ *  - Return value: 0 = ok, < 0 = error (see KPL_E*); kpl_last_error()
+ *    returns a static message for the most recent error on the calling thread.
+ *  - All launches are asynchronous on `stream`; nothing synchronises except
+ *    kpl_read_status() (one 128-byte device->host copy).
+ *  - Floating-point: fp64 everywhere, compiled with --fmad=false, so every
+ *    elementwise operation rounds exactly like the reference's numpy ufuncs.
+ *  - Reductions use the deterministic tile/chunk tree order documented in
+ *    DESIGN.md ("Reduction order"); kpl_reduction_layout() reports the
+ *    parameters so a CPU emulation can reproduce it bit for bit.
+ */
+#ifndef KPL_B200_H
+#define KPL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ------------------------------------------------------- */
+#define KPL_OK              0
+#define KPL_EINVAL         -1   /* invalid argument (reference: ValueError)      */
+#define KPL_ECUDA          -2   /* CUDA runtime error                            */
+#define KPL_EUNSUPPORTED   -3   /* combination not built                          */
+
+/* ---- operator description --------------------------------------------- */
+#define KPL_OP_STENCIL   1   /* unscaled Dirichlet Laplacian, matrix-free         */
+#define KPL_OP_CSR       2   /* CSR, int32 row_ptr/col_idx, fp64 values           */
+
+#define KPL_PC_IDENTITY     0   /* precond.py:84-85  apply returns v              */
+#define KPL_PC_JACOBI_CONST 1   /* precond.py:88-89  v * inv_diag, inv_diag == c  */
+#define KPL_PC_JACOBI_VEC   2   /* precond.py:88-89  v * inv_diag[k]              */
+
+typedef struct kpl_op {
+    int32_t kind;            /* KPL_OP_*                                         */
+    int32_t precond;         /* KPL_PC_*                                         */
+    int64_t n;               /* local rows (this rank)                           */
+    /* stencil: grid (nx, ny, nz), id = x + nx*(y + ny*z); a 2D nx-by-ny grid
+       is (nx, 1, ny).  Off-diagonals are -1, the diagonal is `diag`.        */
+    int64_t nx, ny, nz;      /* local grid (nz = planes owned by this rank)      */
+    double  diag;
+    int32_t zc;              /* planes per reduction chunk (0 = library default) */
+    int32_t vx;              /* 0 = auto, 1 or 2 elements per thread along x     */
+    /* z-slab halos of the stencil input (multi-GPU; NULL = Dirichlet ghost).
+       Each holds one plane of nx*ny raw input values.                      */
+    const double *halo_lo;   /* plane z = -1 of the current stencil input        */
+    const double *halo_hi;   /* plane z = nz                                     */
+    /* csr                                                                   */
+    const int32_t *row_ptr;  /* n+1 local offsets                                */
+    const int32_t *col_idx;  /* global column ids (single GPU: local)           */
+    const double  *values;
+    int64_t nnz;
+    int32_t chunk_blocks;    /* 256-row blocks per reduction chunk (0 = default) */
+    int32_t _pad0;
+    /* preconditioner                                                        */
+    double  pc_const;        /* KPL_PC_JACOBI_CONST                              */
+    const double *inv_diag;  /* KPL_PC_JACOBI_VEC, length n (gathered via col)   */
+    /* multi-GPU reduction: this rank's first global chunk, total chunks
+       (0 = single GPU: the last CTA finalises inline)                       */
+    int64_t chunk_offset;
+    int64_t chunks_global;
+} kpl_op;
+
+/* ---- solver configuration (mirror of SolverConfig, solvers.py:60-86) ---- */
+#define KPL_M_CG      0
+#define KPL_M_PCG     1
+#define KPL_M_PCG_SH  2
+#define KPL_M_PCG_RR  4
+
+typedef struct kpl_cfg {
+    int32_t method;          /* KPL_M_*                                          */
+    int32_t _pad0;
+    double  shift;           /* sigma (pcg_sh)                                    */
+    int64_t max_iters;
+    double  rtol;
+    double  rr_threshold;    /* tau (pcg_rr)                                      */
+    double  rr_coef;         /* (mu*sqrt(n)+1)*norm_inf(A)  (solvers.py:514)      */
+} kpl_cfg;
+
+/* Solver vectors (device, length n).  With KPL_PC_IDENTITY the reference's
+   u, q, p are bitwise copies of r, s, t (precond.py:84-85 returns the same
+   object), so pass u=r, q=s, p=t and the kernels skip them.  `w0`/`w1` are
+   the ping-pong buffers of w (the stencil input is read at neighbours while
+   the next w is written); `p0`/`p1` likewise for classic CG's direction.  */
+typedef struct kpl_vecs {
+    double *x, *r, *u, *w0, *w1, *z, *q, *s, *t, *p, *p1;
+    const double *b;
+} kpl_vecs;
+
+/* Device status, copied to the host by kpl_read_status (16 x 8 bytes). */
+#define KPL_ST_RUNNING    0
+#define KPL_ST_DONE       1
+#define KPL_ST_BREAKDOWN  2
+
+typedef struct kpl_status {
+    int64_t state;           /* KPL_ST_*                                         */
+    int64_t iter;            /* index of the latest history row                  */
+    int64_t converged;
+    int64_t bd_iter;         /* BreakdownError.iteration                         */
+    int64_t bd_code;         /* index into kpl_breakdown_message()               */
+    int64_t n_replacements;  /* pcg_rr                                           */
+    int64_t fire;            /* pcg_rr: replacement pending                      */
+    int64_t _pad[9];
+} kpl_status;
+
+/* History row layout (fp64, 6 columns, row i = record i):
+   alpha, beta, gamma, delta, rnorm_recursive, rnorm_true (NaN = None).     */
+#define KPL_HIST_COLS 6
+
+/* ---- sizing / introspection -------------------------------------------- */
+int64_t kpl_workspace_bytes(const kpl_op *op, int64_t max_iters);
+/* byte offsets of the history table / replacement list inside the workspace */
+int64_t kpl_history_offset(const kpl_op *op);
+int64_t kpl_replacements_offset(const kpl_op *op, int64_t max_iters);
+/* Reduction layout: out[0..7] = {vx, wx, wy, zc, tiles_x, tiles_y, chunks,
+   items_per_chunk} for stencils; {1, 256, 1, chunk_blocks, 0, 0, chunks,
+   chunk_blocks} for CSR.                                                  */
+int kpl_reduction_layout(const kpl_op *op, int64_t *out8);
+const char *kpl_last_error(void);
+const char *kpl_breakdown_message(int64_t code);
+int kpl_version(void);
+/* Number of kernels this library has launched in the process (bench evidence). */
+int64_t kpl_launch_count(void);
+
+/* ---- level-1/2 kernels (reference: sparse.py / _kernels.py) ------------ */
+/* out = A v                    -- sparse.py:153-160 -> _kernels.py:44-52     */
+int kpl_spmv(const kpl_op *op, const double *v, double *out, void *stream);
+/* *result = (u, v), deterministic tree order -- sparse.py:163-169 ->
+   _kernels.py:15-41.  `result` is a device double.                          */
+int kpl_dot(const kpl_op *op, const double *u, const double *v, double *result,
+            void *workspace, void *stream);
+/* out = alpha*x + y, alpha == 0 -> exact copy of y -- sparse.py:172-180      */
+int kpl_axpy(int64_t n, double alpha, const double *x, const double *y, double *out,
+             void *stream);
+
+/* ---- solver (reference: solvers.py solve_* loop bodies) ---------------- */
+/* Initialise workspace + vectors: bnorm = ||b||, x = x0 (NULL -> 0),
+   r = b - A x, u = M r, w = A u - sigma r, z=q=s=t=p=0, history row 0 and
+   (alpha_0, beta_0).  Reference: solvers.py:369-393 (pcg_sh), :306-329
+   (pcg), :246-285 (cg), :545-571 (pcg_rr).                                 */
+int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
+                    const double *x0, void *workspace, void *stream);
+/* Enqueue `count` iterations starting at nominal index `first`
+   (host's count of updates issued).  Each is a predicated no-op once the
+   device status leaves RUNNING.  Reference: one pass of the loop body
+   solvers.py:387-421 (pcg_sh) -- n = A M^-1 w, the nine recurrences and the
+   next (gamma, delta, ||r||) fused into one sweep -- plus the true-residual
+   cadence of solvers.py:233-234 before every update whose index is a
+   multiple of 10.                                                          */
+int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
+                       int64_t first, int64_t count, void *workspace, void *stream);
+/* Classic CG in two halves so a host callback can observe the record
+   point (solvers.py:286-287): pass 1 = true-residual cadence + p, s = A p,
+   delta, record; pass 2 = x, r, u updates and the next head.               */
+int kpl_solver_cg_pass(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, int64_t j,
+                       int32_t pass, void *workspace, void *stream);
+/* After the device reports DONE: ||b - A x|| for the final record if the
+   cadence did not already produce it (solvers.py:401-402, `last`).          */
+int kpl_solver_finish(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
+                      void *workspace, void *stream);
+/* Synchronous copy of the device status to host memory `out`.               */
+int kpl_read_status(const void *workspace, kpl_status *out, void *stream);
+
+/* ---- multi-GPU hooks (one process per GPU; host drives NCCL) ----------- */
+/* Level-4 reduction + scalar update after the chunk partials of all ranks
+   have been gathered into the workspace's global chunk table.  `phase`
+   names the sweep whose partials are pending (returned by
+   kpl_pending_phase).                                                      */
+int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfg, void *workspace,
+                        void *stream);
+/* Device pointer + byte size of this rank's slice of the chunk table and of
+   the whole table (for ncclAllGather).                                      */
+int kpl_chunk_table(const kpl_op *op, void *workspace, void **local, void **global,
+                    int64_t *local_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KPL_B200_H */

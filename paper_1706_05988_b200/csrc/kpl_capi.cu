@@ -1,0 +1,507 @@
+// kpl_capi.cu -- extern "C" entry points of libkpl_b200.so (include/kpl_b200.h).
+//
+// Host side: layout selection, workspace carving, template dispatch on
+// (operator kind, vector width, preconditioner), and the per-iteration
+// launch sequences of the four solvers.  No allocation, no synchronisation
+// except kpl_read_status.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <atomic>
+#include <algorithm>
+
+#include "kpl_bodies.cuh"
+#include "kpl_sweep.cuh"
+
+using namespace kpl;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};   // kernels this library has launched (bench evidence)
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_check(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(KPL_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return KPL_OK;
+}
+
+long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+long long align256(long long v) { return (v + 255) & ~255LL; }
+
+constexpr int kSMs = 148;
+
+int make_layout(const kpl_op *op, Layout &L) {
+    if (!op) return fail(KPL_EINVAL, "null operator");
+    std::memset(&L, 0, sizeof(L));
+    if (op->kind == KPL_OP_STENCIL) {
+        if (op->nx < 1 || op->ny < 1 || op->nz < 1) return fail(KPL_EINVAL, "grid dimensions must be >= 1");
+        if (op->n != op->nx * op->ny * op->nz) return fail(KPL_EINVAL, "n != nx*ny*nz");
+        int vx = op->vx ? op->vx : ((op->nx % 2 == 0) ? 2 : 1);
+        if (vx != 1 && vx != 2) return fail(KPL_EINVAL, "vx must be 1 or 2");
+        if (vx == 2 && (op->nx % 2)) return fail(KPL_EINVAL, "vx=2 needs an even nx");
+        L.vx = vx;
+        if (op->ny == 1) { L.wx = NWARP; L.wy = 1; } else { L.wx = 1; L.wy = NWARP; }
+        const long long TX = 32LL * vx * L.wx, TY = L.wy;
+        L.ntx = (int)cdiv(op->nx, TX);
+        L.nty = (int)cdiv(op->ny, TY);
+        L.T = L.ntx * L.nty;
+        int zc = op->zc;
+        if (zc <= 0) {
+            zc = 16;   // shrink until the grid has >= 4 CTAs per SM
+            while (zc > 1 && (long long)L.T * cdiv(op->nz, zc) < 4LL * kSMs) zc >>= 1;
+        }
+        L.zc = zc;
+        L.nch = cdiv(op->nz, zc);
+        L.items = L.nch * L.T;
+        return KPL_OK;
+    }
+    if (op->kind == KPL_OP_CSR) {
+        if (op->n < 1) return fail(KPL_EINVAL, "matrix dimension must be >= 1");
+        // row_ptr == NULL describes a plain vector (dot / axpy layout, no SpMV)
+        if (op->row_ptr && ((!op->col_idx && op->nnz) || (!op->values && op->nnz)))
+            return fail(KPL_EINVAL, "CSR arrays missing");
+        const long long blocks = cdiv(op->n, RB);
+        const int cb = op->chunk_blocks > 0 ? op->chunk_blocks : 16;
+        L.vx = 1; L.wx = NWARP; L.wy = 1; L.zc = cb;
+        L.T = cb;
+        L.items = blocks;
+        L.nch = cdiv(blocks, cb);
+        return KPL_OK;
+    }
+    return fail(KPL_EINVAL, "unknown operator kind");
+}
+
+struct Offsets { long long items, chunks, cnt, hist, reps, total; };
+
+Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
+    Offsets o;
+    const long long cg = op->chunks_global > 0 ? op->chunks_global : L.nch;
+    o.items = 1024;
+    o.chunks = o.items + align256(8LL * NQ * L.items);
+    o.cnt = o.chunks + align256(8LL * NQ * cg);
+    o.hist = o.cnt + align256(4LL * L.nch);
+    o.reps = o.hist + align256(48LL * (max_iters + 1));
+    o.total = o.reps + align256(8LL * (max_iters + 1));
+    return o;
+}
+
+Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspace) {
+    const Offsets o = offsets(op, L, max_iters);
+    char *base = static_cast<char *>(workspace);
+    Ws ws;
+    ws.head = reinterpret_cast<WsHead *>(base);
+    ws.items = reinterpret_cast<double *>(base + o.items);
+    ws.chunks = reinterpret_cast<double *>(base + o.chunks);
+    ws.chunk_cnt = reinterpret_cast<unsigned int *>(base + o.cnt);
+    ws.hist = reinterpret_cast<double *>(base + o.hist);
+    ws.reps = reinterpret_cast<long long *>(base + o.reps);
+    ws.chunk_offset = op->chunks_global > 0 ? op->chunk_offset : 0;
+    ws.chunks_global = op->chunks_global > 0 ? op->chunks_global : L.nch;
+    ws.inline_final = op->chunks_global > 0 ? 0 : 1;
+    return ws;
+}
+
+Cfg make_cfg(const kpl_cfg *c) {
+    Cfg k;
+    k.method = c ? c->method : KPL_M_PCG_SH;
+    k.shift = c ? c->shift : 0.0;
+    k.rtol = c ? c->rtol : 0.0;
+    k.tau = c ? c->rr_threshold : 0.0;
+    k.coef = c ? c->rr_coef : 0.0;
+    k.max_iters = c ? c->max_iters : 0;
+    return k;
+}
+
+// ------------------------------------------------------------ dispatch
+template <class In, class Body>
+int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, const Cfg &cfg,
+           int phase, int pred, long long row, cudaStream_t st) {
+    if (L.items <= 0) return KPL_OK;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (op->kind == KPL_OP_STENCIL) {
+        SGeo g{op->nx, op->ny, op->nz, op->diag, op->halo_lo, op->halo_hi};
+        if (L.vx == 2)
+            stencil_sweep<2, In, Body><<<(unsigned)L.items, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
+        else
+            stencil_sweep<1, In, Body><<<(unsigned)L.items, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
+    } else {
+        CGeo g{op->n, op->row_ptr, op->col_idx, op->values};
+        csr_sweep<In, Body><<<(unsigned)L.items, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
+    }
+    return cuda_check("sweep launch");
+}
+
+template <int PC>
+InVec<PC> in_vec(const kpl_op *op, const double *a0, const double *a1, int sel) {
+    InVec<PC> in;
+    in.a0 = a0; in.a1 = a1; in.sel = sel; in.c = op->pc_const; in.dinv = op->inv_diag; in.a = a0;
+    return in;
+}
+
+// Calls f(std::integral_constant<int, PC>) for the operator's preconditioner.
+template <class F>
+int with_pc(const kpl_op *op, F &&f) {
+    if (op->kind == KPL_OP_STENCIL) {
+        if (op->precond == KPL_PC_IDENTITY) return f(std::integral_constant<int, KPL_PC_IDENTITY>());
+        if (op->precond == KPL_PC_JACOBI_CONST) return f(std::integral_constant<int, KPL_PC_JACOBI_CONST>());
+        return fail(KPL_EUNSUPPORTED, "stencil operators take identity or constant-diagonal Jacobi");
+    }
+    if (op->precond == KPL_PC_IDENTITY) return f(std::integral_constant<int, KPL_PC_IDENTITY>());
+    if (op->precond == KPL_PC_JACOBI_VEC) {
+        if (!op->inv_diag) return fail(KPL_EINVAL, "Jacobi needs inv_diag");
+        return f(std::integral_constant<int, KPL_PC_JACOBI_VEC>());
+    }
+    return fail(KPL_EUNSUPPORTED, "CSR operators take identity or vector Jacobi");
+}
+
+__global__ void head_init_kernel(WsHead *h, double *hist, long long nrows, unsigned int *cnt, long long ncnt) {
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (tid == 0) {
+        h->state = KPL_ST_RUNNING;
+        h->iter = -1;
+        h->converged = 0;
+        h->bd_iter = -1;
+        h->bd_code = 0;
+        h->n_rep = 0;
+        h->fire = 0;
+        h->alpha = 0.0;
+        h->beta = 0.0;
+        h->gamma_prev = 0.0;    // solvers.py:382
+        h->alpha_prev = 1.0;    // solvers.py:383
+        h->final_cnt = 0u;
+        h->cg_gamma = 0.0;
+    }
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    for (long long k = tid; k < nrows * 6; k += gridDim.x * (long long)blockDim.x) hist[k] = nan;
+    for (long long k = tid; k < ncnt; k += gridDim.x * (long long)blockDim.x) cnt[k] = 0u;
+}
+
+__global__ void axpy_kernel(long long n, double a, const double *__restrict__ x, const double *__restrict__ y,
+                            double *__restrict__ out) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += gridDim.x * (long long)blockDim.x)
+        out[k] = axpy1(a, x[k], y[k]);
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+int kpl_version(void) { return 1; }
+
+int64_t kpl_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char *kpl_last_error(void) { return g_err.c_str(); }
+
+const char *kpl_breakdown_message(int64_t code) {
+    switch (code) {
+    case BD_NONPOS_RU: return "nonpositive (r, u)";
+    case BD_NONPOS_WU: return "nonpositive curvature (w, u)";
+    case BD_VANISH_RU: return "vanishing (r, u)";
+    case BD_VANISH_DEN: return "vanishing alpha denominator";
+    case BD_NONFINITE: return "non-finite coefficients";
+    case BD_NONPOS_SP: return "nonpositive curvature (s, p)";
+    default: return "";
+    }
+}
+
+int64_t kpl_workspace_bytes(const kpl_op *op, int64_t max_iters) {
+    Layout L;
+    if (make_layout(op, L) != KPL_OK) return KPL_EINVAL;
+    return offsets(op, L, max_iters < 0 ? 0 : max_iters).total;
+}
+
+int64_t kpl_history_offset(const kpl_op *op) {
+    Layout L;
+    if (make_layout(op, L) != KPL_OK) return KPL_EINVAL;
+    return offsets(op, L, 0).hist;
+}
+
+int64_t kpl_replacements_offset(const kpl_op *op, int64_t max_iters) {
+    Layout L;
+    if (make_layout(op, L) != KPL_OK) return KPL_EINVAL;
+    return offsets(op, L, max_iters).reps;
+}
+
+int kpl_reduction_layout(const kpl_op *op, int64_t *out8) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if (op->kind == KPL_OP_STENCIL) {
+        const int64_t v[8] = {L.vx, L.wx, L.wy, L.zc, L.ntx, L.nty, L.nch, L.T};
+        std::memcpy(out8, v, sizeof(v));
+    } else {
+        const int64_t v[8] = {1, RB, 1, L.zc, 0, 0, L.nch, L.T};
+        std::memcpy(out8, v, sizeof(v));
+    }
+    return KPL_OK;
+}
+
+static int need_matrix(const kpl_op *op) {
+    if (op->kind == KPL_OP_CSR && !op->row_ptr) return fail(KPL_EINVAL, "CSR arrays missing");
+    return KPL_OK;
+}
+
+int kpl_spmv(const kpl_op *op, const double *v, double *out, void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if ((rc = need_matrix(op)) != KPL_OK) return rc;
+    Ws ws{};
+    Cfg cfg{};
+    BodySpmv body;
+    body.out = out;
+    InVec<KPL_PC_IDENTITY> in = in_vec<KPL_PC_IDENTITY>(op, v, v, SEL_FIXED);
+    return launch(op, L, in, body, ws, cfg, PH_NONE, PRED_ALWAYS, 0, (cudaStream_t)stream);
+}
+
+int kpl_dot(const kpl_op *op, const double *u, const double *v, double *result, void *workspace,
+            void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if (!workspace) return fail(KPL_EINVAL, "workspace required");
+    cudaStream_t st = (cudaStream_t)stream;
+    Ws ws = make_ws(op, L, 0, workspace);
+    Cfg cfg{};
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    head_init_kernel<<<1, 256, 0, st>>>(ws.head, ws.hist, 0, ws.chunk_cnt, L.nch);
+    BodyDot body;
+    body.a = u; body.b = v;
+    rc = launch(op, L, InNone(), body, ws, cfg, PH_DOT, PRED_ALWAYS, 0, st);
+    if (rc != KPL_OK) return rc;
+    if (result) {
+        cudaMemcpyAsync(result, &ws.head->dot_result, sizeof(double), cudaMemcpyDeviceToDevice, st);
+        return cuda_check("dot result copy");
+    }
+    return KPL_OK;
+}
+
+int kpl_axpy(int64_t n, double alpha, const double *x, const double *y, double *out, void *stream) {
+    if (n < 0) return fail(KPL_EINVAL, "negative length");
+    if (n == 0) return KPL_OK;
+    const long long blocks = std::min<long long>(cdiv(n, 256), 148LL * 16);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    axpy_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(n, alpha, x, y, out);
+    return cuda_check("axpy");
+}
+
+int kpl_read_status(const void *workspace, kpl_status *out, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemcpyAsync(out, workspace, sizeof(kpl_status), cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(KPL_ECUDA, std::string("status read: ") + cudaGetErrorString(e));
+    return KPL_OK;
+}
+
+int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, const double *x0,
+                    void *workspace, void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if (!cfgp || !v || !workspace) return fail(KPL_EINVAL, "null argument");
+    if ((rc = need_matrix(op)) != KPL_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Cfg cfg = make_cfg(cfgp);
+    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
+    const long long n = op->n;
+    const bool ident = op->precond == KPL_PC_IDENTITY;
+    const double sigma = cfg.method == KPL_M_PCG_SH ? cfg.shift : 0.0;
+
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    head_init_kernel<<<64, 256, 0, st>>>(ws.head, ws.hist, cfg.max_iters + 1, ws.chunk_cnt, L.nch);
+    if ((rc = cuda_check("head init")) != KPL_OK) return rc;
+
+    // bnorm = norm2(b)  (solvers.py:372)
+    {
+        BodyDot body;
+        body.a = v->b; body.b = v->b;
+        if ((rc = launch(op, L, InNone(), body, ws, cfg, PH_BNORM, PRED_ALWAYS, 0, st)) != KPL_OK) return rc;
+    }
+    // x = x0.copy(); r = b - A x; u = M r   (solvers.py:373-375)
+    const double *xin = x0;
+    int copy_x = 1;
+    if (!x0) {
+        cudaMemsetAsync(v->x, 0, sizeof(double) * n, st);
+        xin = v->x;
+        copy_x = 0;
+    } else if (x0 == v->x) {
+        copy_x = 0;
+    }
+    rc = with_pc(op, [&](auto pc) -> int {
+        constexpr int PC = decltype(pc)::value;
+        BodyInitR<PC> body;
+        body.b = v->b; body.x = v->x; body.r = v->r; body.u = v->u;
+        body.dinv = op->inv_diag; body.c = op->pc_const; body.copy_x = copy_x;
+        return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, xin, xin, SEL_FIXED), body, ws, cfg,
+                      PH_INITR, PRED_ALWAYS, 0, st);
+    });
+    if (rc != KPL_OK) return rc;
+    const double *u = ident ? v->r : v->u;
+
+    if (cfg.method == KPL_M_CG) {
+        cudaMemsetAsync(v->p, 0, sizeof(double) * n, st);      // p = zeros (solvers.py:252)
+        return cuda_check("cg init");
+    }
+    // z = q = s = t = p = 0 (solvers.py:377-381); w = axpy(-sigma, r, A u) (:376)
+    cudaMemsetAsync(v->z, 0, sizeof(double) * n, st);
+    cudaMemsetAsync(v->s, 0, sizeof(double) * n, st);
+    cudaMemsetAsync(v->t, 0, sizeof(double) * n, st);
+    if (!ident) {
+        cudaMemsetAsync(v->q, 0, sizeof(double) * n, st);
+        cudaMemsetAsync(v->p, 0, sizeof(double) * n, st);
+    }
+    BodyInitW body;
+    body.r = v->r; body.u = u; body.w = v->w0; body.sigma = sigma; body.ident = ident;
+    return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, u, u, SEL_FIXED), body, ws, cfg, PH_PIPE,
+                  PRED_ALWAYS, 0, st);
+}
+
+// One true-residual sweep for history row `row` (predicated on iter == row).
+static int true_residual(const kpl_op *op, const Layout &L, const kpl_vecs *v, const Ws &ws, const Cfg &cfg,
+                         long long row, int pred, cudaStream_t st) {
+    BodyTrue body;
+    body.b = v->b;
+    return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), body, ws, cfg, PH_TRUE, pred,
+                  row, st);
+}
+
+int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t first,
+                       int64_t count, void *workspace, void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if (!cfgp || !v || !workspace) return fail(KPL_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const Cfg cfg = make_cfg(cfgp);
+    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
+    const bool ident = op->precond == KPL_PC_IDENTITY;
+    const double sigma = cfg.method == KPL_M_PCG_SH ? cfg.shift : 0.0;
+
+    for (int64_t j = first; j < first + count; ++j) {
+        if (j % 10 == 0) {
+            if ((rc = true_residual(op, L, v, ws, cfg, j, PRED_ROW, st)) != KPL_OK) return rc;
+        }
+        if (cfg.method == KPL_M_CG) {
+            rc = with_pc(op, [&](auto pc) -> int {
+                constexpr int PC = decltype(pc)::value;
+                InCgP in;
+                in.p0 = v->p; in.p1 = v->p1; in.u = ident ? v->r : v->u; in.p = v->p; in.beta = 0.0;
+                BodyCgP bp;
+                bp.p0 = v->p; bp.p1 = v->p1; bp.s = v->s; bp.pout = v->p1;
+                int r2 = launch(op, L, in, bp, ws, cfg, PH_CGDELTA, PRED_RUNNING, 0, st);
+                if (r2 != KPL_OK) return r2;
+                BodyCgX<PC> bx;
+                bx.x = v->x; bx.r = v->r; bx.u = v->u; bx.p0 = v->p; bx.p1 = v->p1; bx.s = v->s;
+                bx.dinv = op->inv_diag; bx.c = op->pc_const; bx.alpha = 0.0; bx.p = v->p;
+                return launch(op, L, InNone(), bx, ws, cfg, PH_CGHEAD, PRED_RUNNING, 0, st);
+            });
+            if (rc != KPL_OK) return rc;
+            continue;
+        }
+        rc = with_pc(op, [&](auto pc) -> int {
+            constexpr int PC = decltype(pc)::value;
+            BodyPcgIter<PC> body;
+            body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
+            body.s = v->s; body.t = v->t; body.p = v->p; body.w0 = v->w0; body.w1 = v->w1;
+            body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = sigma;
+            body.want_xi = cfg.method == KPL_M_PCG_RR;
+            body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
+            int r2 = launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, ws, cfg, PH_PIPE,
+                            PRED_RUNNING, 0, st);
+            if (r2 != KPL_OK || cfg.method != KPL_M_PCG_RR) return r2;
+            // explicit replacement, predicated on the device trigger (solvers.py:599-607)
+            const double *uu = ident ? v->r : v->u;
+            BodyInitR<PC> r1;
+            r1.b = v->b; r1.x = v->x; r1.r = v->r; r1.u = v->u; r1.dinv = op->inv_diag;
+            r1.c = op->pc_const; r1.copy_x = 0;
+            if ((r2 = launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), r1, ws, cfg, PH_NONE,
+                             PRED_FIRE, 0, st)) != KPL_OK) return r2;
+            BodyRepl<PC> rw;
+            rw.mode = 0; rw.w0 = v->w0; rw.w1 = v->w1; rw.s = v->s; rw.q = v->q; rw.dinv = op->inv_diag;
+            rw.c = op->pc_const; rw.wout = v->w1;
+            if ((r2 = launch(op, L, in_vec<KPL_PC_IDENTITY>(op, uu, uu, SEL_FIXED), rw, ws, cfg, PH_NONE,
+                             PRED_FIRE, 0, st)) != KPL_OK) return r2;
+            BodyRepl<PC> rs = rw;
+            rs.mode = 1;
+            const double *pp = ident ? v->t : v->p;
+            if ((r2 = launch(op, L, in_vec<KPL_PC_IDENTITY>(op, pp, pp, SEL_FIXED), rs, ws, cfg, PH_NONE,
+                             PRED_FIRE, 0, st)) != KPL_OK) return r2;
+            BodyReplZ rz;
+            rz.z = v->z; rz.r = v->r; rz.u = uu; rz.w0 = v->w0; rz.w1 = v->w1; rz.ident = ident; rz.w = v->w0;
+            const double *qq = ident ? v->s : v->q;
+            return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, qq, qq, SEL_FIXED), rz, ws, cfg, PH_RRFINAL,
+                          PRED_FIRE, 0, st);
+        });
+        if (rc != KPL_OK) return rc;
+    }
+    return KPL_OK;
+}
+
+int kpl_solver_cg_pass(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t j, int32_t pass,
+                       void *workspace, void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if (!cfgp || !v || !workspace) return fail(KPL_EINVAL, "null argument");
+    if (cfgp->method != KPL_M_CG) return fail(KPL_EINVAL, "cg_pass is for classic CG");
+    cudaStream_t st = (cudaStream_t)stream;
+    const Cfg cfg = make_cfg(cfgp);
+    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
+    const bool ident = op->precond == KPL_PC_IDENTITY;
+    if (pass == 1) {
+        if (j % 10 == 0 && (rc = true_residual(op, L, v, ws, cfg, j, PRED_ROW, st)) != KPL_OK) return rc;
+        InCgP in;
+        in.p0 = v->p; in.p1 = v->p1; in.u = ident ? v->r : v->u; in.p = v->p; in.beta = 0.0;
+        BodyCgP bp;
+        bp.p0 = v->p; bp.p1 = v->p1; bp.s = v->s; bp.pout = v->p1;
+        return launch(op, L, in, bp, ws, cfg, PH_CGDELTA, PRED_RUNNING, 0, st);
+    }
+    return with_pc(op, [&](auto pc) -> int {
+        constexpr int PC = decltype(pc)::value;
+        BodyCgX<PC> bx;
+        bx.x = v->x; bx.r = v->r; bx.u = v->u; bx.p0 = v->p; bx.p1 = v->p1; bx.s = v->s;
+        bx.dinv = op->inv_diag; bx.c = op->pc_const; bx.alpha = 0.0; bx.p = v->p;
+        return launch(op, L, InNone(), bx, ws, cfg, PH_CGHEAD, PRED_RUNNING, 0, st);
+    });
+}
+
+int kpl_solver_finish(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, void *workspace,
+                      void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Cfg cfg = make_cfg(cfgp);
+    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
+    kpl_status s;
+    if ((rc = kpl_read_status(workspace, &s, stream)) != KPL_OK) return rc;
+    if (s.state != KPL_ST_DONE) return KPL_OK;
+    if (s.iter % 10 == 0) return KPL_OK;      // cadence already produced it
+    return true_residual(op, L, v, ws, cfg, s.iter, PRED_ROW, st);
+}
+
+int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfgp, void *workspace, void *stream) {
+    (void)op; (void)cfgp; (void)workspace; (void)stream;
+    return fail(KPL_EUNSUPPORTED, "multi-GPU finalize: not built in this round");
+}
+
+int kpl_chunk_table(const kpl_op *op, void *workspace, void **local, void **global, int64_t *local_bytes) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    Ws ws = make_ws(op, L, 0, workspace);
+    if (global) *global = ws.chunks;
+    if (local) *local = ws.chunks + ws.chunk_offset * NQ;
+    if (local_bytes) *local_bytes = 8LL * NQ * L.nch;
+    return KPL_OK;
+}
+
+}  // extern "C"

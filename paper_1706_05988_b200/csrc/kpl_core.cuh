@@ -1,0 +1,415 @@
+// kpl_core.cuh -- device-side building blocks shared by every sweep:
+// workspace layout, streaming loads/stores, the deterministic reduction tree,
+// and the scalar recurrences of the reference solvers.
+//
+// Compiled with --fmad=false: every a*b+c below is two IEEE roundings, the
+// same as the reference's numba kernels and numpy ufuncs.
+// The hot update formulas additionally use __dmul_rn/__dadd_rn/__dsub_rn so
+// contraction is impossible even if the flag were dropped.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/kpl_b200.h"
+
+namespace kpl {
+
+constexpr int NT = 256;          // threads per CTA for every sweep
+constexpr int NWARP = NT / 32;   // 8 warps
+constexpr int NQ = 4;            // reduced quantities per item (max)
+constexpr int RB = 256;          // CSR rows per item (one row per thread)
+
+// ---------------------------------------------------------------- workspace
+// Offset 0: head (1 KiB).  Mirrors kpl_status in its first 16 int64.
+struct WsHead {
+    long long state, iter, converged, bd_iter, bd_code, n_rep, fire, _st_pad[9];
+    double alpha, beta, gamma_prev, alpha_prev;  // pipelined coefficients
+    double bnorm, dot_result;
+    double rr_e, rr_xnorm;                        // residual-replacement trigger
+    long long rr_held, rr_started;
+    double cg_gamma, cg_beta, cg_rnorm, cg_alpha; // classic CG head -> delta
+    long long cg_last, _cg_pad;
+    double dsig_pad[4];
+    unsigned int final_cnt, _cnt_pad[7];
+};
+static_assert(sizeof(WsHead) <= 1024, "head too large");
+
+enum Phase : int {
+    PH_NONE = 0,      // no reduction (spmv, replacement intermediates)
+    PH_DOT = 1,       // result -> head.dot_result
+    PH_BNORM = 2,     // head.bnorm = sqrt(v0)
+    PH_INITR = 3,     // r = b - A x0: pcg_rr trigger.start(|x|, |r|)  (+ CG head of row 0)
+    PH_PIPE = 4,      // pipelined record: gamma, delta, rho (+xi for rr)
+    PH_RRFINAL = 5,   // after an explicit replacement: trigger.reset + record
+    PH_TRUE = 6,      // ||b - A x|| into the current history row
+    PH_CGHEAD = 7,    // classic CG: gamma, rho -> beta, convergence, last
+    PH_CGDELTA = 8,   // classic CG: delta -> alpha, record, done
+};
+
+// Launch predicate evaluated uniformly by every CTA at kernel start.
+enum Pred : int {
+    PRED_ALWAYS = 0,
+    PRED_RUNNING = 1,        // state == RUNNING
+    PRED_FIRE = 2,           // state == RUNNING && fire  (pcg_rr replacement)
+    PRED_ROW = 3,            // head.iter == row (explicit true-residual row)
+    PRED_CADENCE = 4,        // head.iter % 10 == 0 and state == RUNNING (graph mode)
+};
+
+struct Layout {               // identical on host and device
+    int vx, wx, wy, zc;       // stencil tile: TX = 32*vx*wx, TY = wy
+    int ntx, nty;             // tiles per plane
+    long long nch;            // chunks owned by this launch (local)
+    long long items;          // CTAs of a sweep
+    int T;                    // items per chunk
+};
+
+struct Ws {                   // device view of the caller's workspace
+    WsHead *head;
+    double *items;            // [items][NQ]
+    double *chunks;           // [chunks_global][NQ] (global table)
+    unsigned int *chunk_cnt;  // [nch_local]
+    double *hist;             // [max_iters+1][6]
+    long long *reps;          // [max_iters+1]
+    long long chunk_offset;   // first global chunk of this rank
+    long long chunks_global;
+    int inline_final;         // 1: last CTA finalises (single GPU)
+};
+
+struct Cfg {                  // scalar view of kpl_cfg
+    int method;
+    double shift, rtol, tau, coef;
+    long long max_iters;
+};
+
+// ------------------------------------------------------------- memory ops
+template <int V> struct Vec;
+template <> struct Vec<1> { using T = double; };
+template <> struct Vec<2> { using T = double2; };
+
+// streaming (evict-first) loads/stores for the vectors touched once per sweep
+template <int V>
+__device__ __forceinline__ void ld_cs(const double *p, long long k, double (&o)[V]) {
+    if constexpr (V == 2) {
+        double2 t = __ldcs(reinterpret_cast<const double2 *>(p + k));
+        o[0] = t.x; o[1] = t.y;
+    } else {
+        o[0] = __ldcs(p + k);
+    }
+}
+template <int V>
+__device__ __forceinline__ void st_cs(double *p, long long k, const double (&o)[V]) {
+    if constexpr (V == 2) {
+        __stcs(reinterpret_cast<double2 *>(p + k), make_double2(o[0], o[1]));
+    } else {
+        __stcs(p + k, o[0]);
+    }
+}
+// read-only loads of the stencil input (re-read by neighbouring tiles: keep in L2)
+template <int V>
+__device__ __forceinline__ void ld_ro(const double *p, long long k, double (&o)[V]) {
+    if constexpr (V == 2) {
+        double2 t = __ldg(reinterpret_cast<const double2 *>(p + k));
+        o[0] = t.x; o[1] = t.y;
+    } else {
+        o[0] = __ldg(p + k);
+    }
+}
+
+// ------------------------------------------------------------ arithmetic
+// axpy(alpha, x, y) of sparse.py:172-180: alpha == 0 -> exact copy of y.
+__device__ __forceinline__ double axpy1(double a, double x, double y) {
+    return a == 0.0 ? y : __dadd_rn(__dmul_rn(a, x), y);
+}
+// _sub2(base, a, xv, c, yv) of solvers.py:170-178.
+__device__ __forceinline__ double sub2(double base, double a, double xv, double c, double yv) {
+    return c == 0.0 ? __dsub_rn(base, __dmul_rn(a, xv))
+                    : __dsub_rn(base, __dadd_rn(__dmul_rn(a, xv), __dmul_rn(c, yv)));
+}
+
+// ------------------------------------------------------- reduction tree
+// Level 2b: xor butterfly over the 32 lanes (every lane ends with the sum).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
+// Level 2c: the NWARP warp totals combined by a halving tree (s[0:4]+s[4:8], ...).
+// Returns the block total in thread 0 (all threads of warp 0 hold it).
+template <int Q>
+__device__ __forceinline__ void block_sum(double (&v)[Q], double *sm /* >= NWARP*Q */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) v[q] = warp_sum(v[q]);
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) sm[q * NWARP + warp] = v[q];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            double t = lane < NWARP ? sm[q * NWARP + lane] : 0.0;
+            t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 4));
+            t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 2));
+            t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 1));
+            v[q] = t;
+        }
+    }
+    __syncthreads();
+}
+
+// Levels 3/4: sum src[j*stride + q] for j in [0, count) -- thread t adds
+// j = t, t+256, ... sequentially from +0.0, then block_sum.  Loads bypass L1
+// (the values were written by other CTAs of this grid).
+template <int Q>
+__device__ __forceinline__ void strided_sum(const double *src, long long count, int stride,
+                                            double (&v)[Q], double *sm) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) v[q] = 0.0;
+    for (long long j = threadIdx.x; j < count; j += NT) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) v[q] = __dadd_rn(v[q], __ldcg(src + j * stride + q));
+    }
+    block_sum<Q>(v, sm);
+}
+
+// ---------------------------------------------------- scalar recurrences
+enum Breakdown : int {
+    BD_NONPOS_RU = 1,        // "nonpositive (r, u)"
+    BD_NONPOS_WU = 2,        // "nonpositive curvature (w, u)"
+    BD_VANISH_RU = 3,        // "vanishing (r, u)"
+    BD_VANISH_DEN = 4,       // "vanishing alpha denominator"
+    BD_NONFINITE = 5,        // "non-finite coefficients"
+    BD_NONPOS_SP = 6,        // "nonpositive curvature (s, p)"
+};
+
+__device__ __forceinline__ void set_breakdown(WsHead *h, long long i, int code) {
+    h->state = KPL_ST_BREAKDOWN;
+    h->bd_iter = i;
+    h->bd_code = code;
+}
+
+// solvers.py:194-230 _pipelined_scalars.  Returns false on breakdown.
+__device__ bool pipelined_scalars(WsHead *h, long long i, double gamma, double delta, bool last,
+                                  double &beta, double &alpha) {
+    const double gamma_prev = h->gamma_prev, alpha_prev = h->alpha_prev;
+    if (i == 0) {
+        beta = 0.0;
+        if (delta > 0.0) {
+            alpha = gamma / delta;
+        } else if (last) {
+            alpha = 0.0;
+        } else if (gamma <= 0.0) {
+            set_breakdown(h, i, BD_NONPOS_RU); return false;
+        } else {
+            set_breakdown(h, i, BD_NONPOS_WU); return false;
+        }
+        return true;
+    }
+    beta = gamma_prev != 0.0 ? gamma / gamma_prev : 0.0;
+    if (last) {
+        if (gamma == 0.0 || delta == 0.0) { alpha = 0.0; return true; }
+        const double denom = __dsub_rn(delta / gamma, beta / alpha_prev);
+        double a = denom != 0.0 ? 1.0 / denom : 0.0;
+        alpha = isfinite(a) ? a : 0.0;
+        return true;
+    }
+    if (gamma == 0.0) { set_breakdown(h, i, BD_VANISH_RU); return false; }
+    const double denom = __dsub_rn(delta / gamma, beta / alpha_prev);
+    if (denom == 0.0) { set_breakdown(h, i, BD_VANISH_DEN); return false; }
+    alpha = 1.0 / denom;
+    if (!(isfinite(alpha) && isfinite(beta))) { set_breakdown(h, i, BD_NONFINITE); return false; }
+    return true;
+}
+
+__device__ __forceinline__ double *hist_row(const Ws &ws, long long i) { return ws.hist + 6 * i; }
+
+__device__ __forceinline__ bool converged_test(const Cfg &cfg, const WsHead *h, double rnorm) {
+    // solvers.py:391
+    return rnorm == 0.0 || (cfg.rtol > 0.0 && rnorm <= cfg.rtol * h->bnorm);
+}
+
+// Pipelined record of row i (solvers.py:388-403 minus the cadence column).
+__device__ void pipe_record(const Ws &ws, const Cfg &cfg, long long i, double gamma, double delta,
+                            double rho) {
+    WsHead *h = ws.head;
+    const double rnorm = sqrt(rho);
+    const bool conv = converged_test(cfg, h, rnorm);
+    const bool last = conv || i == cfg.max_iters;
+    double beta, alpha;
+    if (!pipelined_scalars(h, i, gamma, delta, last, beta, alpha)) return;
+    double *row = hist_row(ws, i);
+    row[0] = alpha; row[1] = beta; row[2] = gamma; row[3] = delta; row[4] = rnorm;
+    h->alpha = alpha;
+    h->beta = beta;
+    h->gamma_prev = gamma;     // solvers.py:420-421 (consumed by row i+1)
+    h->alpha_prev = alpha;
+    h->iter = i;
+    if (last) {
+        h->converged = conv ? 1 : 0;
+        h->state = KPL_ST_DONE;
+    }
+}
+
+// _ReplacementTrigger (solvers.py:501-532); eps = unit roundoff.
+constexpr double UNIT_ROUNDOFF = 1.1102230246251565e-16;
+
+// The scalar epilogue run once per sweep by one thread after the reduction.
+__device__ void finalize(const Ws &ws, const Cfg &cfg, int phase, const double (&v)[NQ]) {
+    WsHead *h = ws.head;
+    switch (phase) {
+    case PH_DOT:
+        h->dot_result = v[0];
+        break;
+    case PH_BNORM:
+        h->bnorm = sqrt(v[0]);
+        break;
+    case PH_INITR: {
+        // v = {(x,x), (r,r), (r,u)}
+        if (cfg.method == KPL_M_PCG_RR) {      // trigger.start (solvers.py:519-521, :558)
+            const double xnorm = sqrt(v[0]), rnorm = sqrt(v[1]);
+            h->rr_e = UNIT_ROUNDOFF * (cfg.coef * xnorm + h->bnorm);
+            h->rr_held = h->rr_e <= cfg.tau * rnorm;
+        }
+        if (cfg.method == KPL_M_CG) {          // classic CG head of row 0 (solvers.py:258-268)
+            const double gamma = v[2], rnorm = sqrt(v[1]);
+            const bool conv = converged_test(cfg, h, rnorm);
+            const bool last = conv || 0 == cfg.max_iters;
+            h->cg_gamma = gamma; h->cg_rnorm = rnorm; h->cg_beta = 0.0;
+            h->cg_last = last; h->converged = conv; h->iter = 0;
+            if (!last && gamma <= 0.0) set_breakdown(h, 0, BD_NONPOS_RU);
+        }
+        break;
+    }
+    case PH_PIPE: {
+        // v = {gamma, delta, rho, xi}; the row index is iter+1 except for init (iter = -1)
+        const long long i = h->iter + 1;
+        if (cfg.method == KPL_M_PCG_RR && i > 0) {   // trigger.update (solvers.py:523-528, :599)
+            const double xnorm = sqrt(v[3]), rnorm = sqrt(v[2]);
+            h->rr_e = h->rr_e + UNIT_ROUNDOFF * (cfg.coef * xnorm + rnorm);
+            const bool ok = h->rr_e <= cfg.tau * rnorm;
+            const bool fire = h->rr_held && !ok && cfg.tau > 0.0;
+            h->rr_held = ok;
+            if (fire) {
+                h->fire = 1;
+                h->rr_xnorm = xnorm;
+                ws.reps[h->n_rep] = i;           // replacements.append(i + 1)
+                h->n_rep += 1;
+                return;                          // record after the replacement sweeps
+            }
+        }
+        pipe_record(ws, cfg, i, v[0], v[1], v[2]);
+        break;
+    }
+    case PH_RRFINAL: {
+        // trigger.reset(|x|, |r|) with the replaced r (solvers.py:530-532, :607)
+        const long long i = h->iter + 1;
+        const double rnorm = sqrt(v[2]);
+        h->rr_e = UNIT_ROUNDOFF * (cfg.coef * h->rr_xnorm + rnorm);
+        h->rr_held = h->rr_e <= cfg.tau * rnorm;
+        h->fire = 0;
+        pipe_record(ws, cfg, i, v[0], v[1], v[2]);
+        break;
+    }
+    case PH_TRUE:
+        hist_row(ws, h->iter)[5] = sqrt(v[0]);
+        break;
+    case PH_CGHEAD: {
+        // v = {(r,u), (r,r)} of the updated vectors: row i = iter + 1 (solvers.py:258-268)
+        const long long i = h->iter + 1;
+        const double gamma = v[0], rnorm = sqrt(v[1]);
+        const bool conv = converged_test(cfg, h, rnorm);
+        const bool last = conv || i == cfg.max_iters;
+        const double gamma_prev = h->cg_gamma;
+        h->cg_beta = gamma_prev > 0.0 ? gamma / gamma_prev : 0.0;
+        h->cg_gamma = gamma; h->cg_rnorm = rnorm;
+        h->cg_last = last; h->converged = conv; h->iter = i;
+        if (!last && gamma <= 0.0) set_breakdown(h, i, BD_NONPOS_RU);
+        break;
+    }
+    case PH_CGDELTA: {
+        // v = {(s,p)} (solvers.py:271-289)
+        const long long i = h->iter;
+        const double delta = v[0], gamma = h->cg_gamma;
+        double alpha;
+        if (h->cg_last) {
+            alpha = delta > 0.0 ? gamma / delta : 0.0;
+        } else if (delta <= 0.0) {
+            set_breakdown(h, i, BD_NONPOS_SP);
+            return;
+        } else {
+            alpha = gamma / delta;
+        }
+        double *row = hist_row(ws, i);
+        row[0] = alpha; row[1] = h->cg_beta; row[2] = gamma; row[3] = delta; row[4] = h->cg_rnorm;
+        h->cg_alpha = alpha;
+        h->alpha = alpha;
+        if (h->cg_last) h->state = KPL_ST_DONE;
+        break;
+    }
+    default:
+        break;
+    }
+}
+
+// Per-kernel uniform predicate.
+__device__ __forceinline__ bool pred_ok(const WsHead *h, int pred, long long row) {
+    switch (pred) {
+    case PRED_RUNNING: return h->state == KPL_ST_RUNNING;
+    case PRED_FIRE: return h->state == KPL_ST_RUNNING && h->fire != 0;
+    case PRED_ROW: return h->iter == row && h->state != KPL_ST_BREAKDOWN;
+    case PRED_CADENCE: return h->state == KPL_ST_RUNNING && (h->iter % 10) == 0;
+    default: return true;
+    }
+}
+
+// After a CTA has written its item partial (thread 0, before the call):
+// chunk-completion and grid-completion counting; the last CTA of a chunk
+// folds the chunk (level 3), the last chunk folds the grid (level 4) and runs
+// the scalar epilogue.  Every CTA of the grid must call this.
+template <int Q>
+__device__ void complete_item(const Ws &ws, const Cfg &cfg, const Layout &L, int phase,
+                              long long chunk_local, double *sm) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    const long long item0 = chunk_local * L.T;
+    const long long expect = min((long long)L.T, L.items - item0);   // last CSR chunk may be short
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&ws.chunk_cnt[chunk_local], 1u);
+        s_last = (prev == (unsigned)(expect - 1));
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double v[Q];
+    strided_sum<Q>(ws.items + item0 * NQ, expect, NQ, v, sm);
+    const long long cg = ws.chunk_offset + chunk_local;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) ws.chunks[cg * NQ + q] = v[q];
+        ws.chunk_cnt[chunk_local] = 0u;
+    }
+    if (!ws.inline_final) return;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
+        s_last = (prev == (unsigned)(L.nch - 1));
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double f[Q];
+    strided_sum<Q>(ws.chunks, ws.chunks_global, NQ, f, sm);
+    if (threadIdx.x == 0) {
+        double full[NQ] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < Q; ++q) full[q] = f[q];
+        finalize(ws, cfg, phase, full);
+        ws.head->final_cnt = 0u;
+        __threadfence();
+    }
+}
+
+}  // namespace kpl

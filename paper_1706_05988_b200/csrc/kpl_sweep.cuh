@@ -1,0 +1,281 @@
+// kpl_sweep.cuh -- the two traversal skeletons every kernel is built from.
+//
+//  * stencil_sweep: one CTA per (x-y tile, z-chunk) item.  8 warps; warp
+//    (wx, wy) owns 32*VX consecutive x-elements of tile row wy.  The CTA
+//    marches through the chunk's planes: the stencil input's own column is a
+//    register queue (z-1, z, z+1, z+2), its x/y neighbours come from a
+//    double-buffered shared-memory plane with a one-element x halo and a
+//    one-row y halo, and the body's streams for plane z+1 are prefetched into
+//    registers while plane z is computed.  One __syncthreads per plane.
+//
+//  * csr_sweep: one CTA per 256-row block.  The block's nonzeros are staged
+//    through shared memory in windows (coalesced loads of values/col_idx,
+//    gather of the input), then each thread sums its own row left to right
+//    from +0.0 -- the reference csr_matvec order (_kernels.py:44-52) -- and
+//    runs the body on that row.
+//
+// Both end with the same deterministic reduction: per-element accumulators
+// (sequential over z for stencils), per-thread pair sum (VX=2), warp xor
+// butterfly, 8-warp halving tree -> item partial; complete_item() folds items
+// into chunks and chunks into the final value.
+#pragma once
+#include "kpl_core.cuh"
+
+namespace kpl {
+
+struct SGeo {
+    long long NX, NY, NZ;
+    double diag;
+    const double *halo_lo, *halo_hi;   // raw stencil-input planes z=-1 / z=NZ (or null)
+};
+
+struct CGeo {
+    long long n;
+    const int *row_ptr, *col_idx;
+    const double *values;
+};
+
+// Largest smem plane: 3D tile (1x8 warps, VX=2): 10 rows x (128+4); 2D tile
+// (8x1 warps, VX=2): 3 rows x (512+4).
+constexpr int SMEM_PLANE = 1548;
+constexpr int CSR_WIN = 2048;      // staged nonzeros per window
+
+template <int VX, class In, class Body>
+__global__ void __launch_bounds__(NT, 2)
+stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
+    constexpr int Q = Body::NQ;
+    __shared__ __align__(16) double sp[Body::kStencil ? 2 : 1][Body::kStencil ? SMEM_PLANE : 2];
+    __shared__ double sred[NQ * NWARP];
+
+    if (!pred_ok(ws.head, pred, row)) return;
+    body.setup(ws);
+    in.setup(ws);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wx = warp % L.wx, wy = warp / L.wx;
+    const int TX = 32 * VX * L.wx, TY = L.wy;
+    const long long item = blockIdx.x;
+    const long long c = item / L.T;
+    const int tile = (int)(item - c * L.T);
+    const int tyi = tile / L.ntx, txi = tile - tyi * L.ntx;
+    const long long x0 = (long long)txi * TX, y0 = (long long)tyi * TY;
+    const int xl = wx * 32 * VX + lane * VX;          // x inside the tile
+    const long long x = x0 + xl, y = y0 + wy;
+    const bool ok = (y < g.NY) && (x < g.NX);         // VX=2 => NX even => pair all-or-none
+    const long long NX = g.NX, sxy = g.NX * g.NY;
+    const long long z0 = c * L.zc;
+    const long long z1 = min(z0 + (long long)L.zc, g.NZ);
+    const int rowlen = TX + 4;                         // [1]=x0-1, [2..TX+1]=tile, [TX+2]=x0+TX
+    const int cidx = (wy + 1) * rowlen + 2 + xl;       // own element in the smem plane
+
+    double acc[Q > 0 ? Q : 1][VX];
+#pragma unroll
+    for (int q = 0; q < (Q > 0 ? Q : 1); ++q)
+#pragma unroll
+        for (int v = 0; v < VX; ++v) acc[q][v] = 0.0;
+
+    // raw stencil-input loaders with Dirichlet ghosts / slab halos
+    auto plane_ptr = [&](long long zz, long long &off) -> const double * {
+        if (zz < 0) { off = 0; return g.halo_lo; }
+        if (zz >= g.NZ) { off = 0; return g.halo_hi; }
+        off = zz * sxy;
+        return in.base();
+    };
+    auto ld_own = [&](long long zz, double (&o)[VX]) {
+#pragma unroll
+        for (int v = 0; v < VX; ++v) o[v] = 0.0;
+        long long off;
+        const double *p = plane_ptr(zz, off);
+        if (ok && p) in.template raw<VX>(p, off + x + NX * y, o);
+    };
+    // halo values of plane zz: [0] x0-1, [1] x0+TX (row y), [2..] y0-1 row, y0+TY row
+    struct Halo { double xl, xr, yl[VX], yh[VX]; };
+    auto ld_halo = [&](long long zz, Halo &hh) {
+        hh.xl = 0.0; hh.xr = 0.0;
+#pragma unroll
+        for (int v = 0; v < VX; ++v) { hh.yl[v] = 0.0; hh.yh[v] = 0.0; }
+        long long off;
+        const double *p = plane_ptr(zz, off);
+        if (!p) return;
+        if (y < g.NY) {
+            if (wx == 0 && lane == 0 && x0 > 0) {
+                double t[1]; in.template raw<1>(p, off + (x0 - 1) + NX * y, t); hh.xl = t[0];
+            }
+            if (wx == L.wx - 1 && lane == 31 && x0 + TX < NX) {
+                double t[1]; in.template raw<1>(p, off + (x0 + TX) + NX * y, t); hh.xr = t[0];
+            }
+        }
+        if (x < NX) {
+            if (wy == 0 && y0 > 0) in.template raw<VX>(p, off + x + NX * (y0 - 1), hh.yl);
+            if (wy == TY - 1 && y0 + TY < g.NY) in.template raw<VX>(p, off + x + NX * (y0 + TY), hh.yh);
+        }
+    };
+    auto stage = [&](double *P, const double (&cen)[VX], const Halo &hh) {
+#pragma unroll
+        for (int v = 0; v < VX; ++v) P[cidx + v] = cen[v];
+        if (wx == 0 && lane == 0) P[(wy + 1) * rowlen + 1] = hh.xl;
+        if (wx == L.wx - 1 && lane == 31) P[(wy + 1) * rowlen + TX + 2] = hh.xr;
+        if (wy == 0) {
+#pragma unroll
+            for (int v = 0; v < VX; ++v) P[2 + xl + v] = hh.yl[v];
+        }
+        if (wy == TY - 1) {
+#pragma unroll
+            for (int v = 0; v < VX; ++v) P[(TY + 1) * rowlen + 2 + xl + v] = hh.yh[v];
+        }
+    };
+
+    typename Body::template Regs<VX> cur, nxt;
+    double qm[VX], qc[VX], qp[VX], qn[VX];
+    Halo h1, h2;
+    if (z0 < z1) {
+        if constexpr (Body::kStencil) {
+            ld_own(z0 - 1, qm);
+            ld_own(z0, qc);
+            ld_own(z0 + 1, qp);
+            Halo h0;
+            ld_halo(z0, h0);
+            ld_halo(z0 + 1, h1);
+            stage(sp[0], qc, h0);
+        }
+        if (ok) body.template load<VX>(z0 * sxy + x + NX * y, cur);
+    }
+    for (long long z = z0; z < z1; ++z) {
+        const int kb = (int)((z - z0) & 1);
+        const long long k = z * sxy + x + NX * y;
+        if constexpr (Body::kStencil) {
+            if (z + 1 < z1) {
+                ld_own(z + 2, qn);
+                ld_halo(z + 2, h2);
+            }
+        }
+        if (z + 1 < z1 && ok) body.template load<VX>(k + sxy, nxt);
+        double n[VX];
+        if constexpr (Body::kStencil) {
+            __syncthreads();
+            const double *P = sp[kb];
+            // terms in ascending column order: z-1, y-1, x-1, diag, x+1, y+1, z+1
+            double ym[VX], yp[VX], xm[VX], xp[VX];
+#pragma unroll
+            for (int v = 0; v < VX; ++v) {
+                ym[v] = P[cidx - rowlen + v];
+                yp[v] = P[cidx + rowlen + v];
+            }
+            xm[0] = P[cidx - 1];
+            xp[VX - 1] = P[cidx + VX];
+            if constexpr (VX == 2) { xm[1] = qc[0]; xp[0] = qc[1]; }
+#pragma unroll
+            for (int v = 0; v < VX; ++v) {
+                const long long kv = k + v;
+                double a = 0.0;
+                a = __dadd_rn(a, -in.xf(qm[v], kv - sxy));
+                a = __dadd_rn(a, -in.xf(ym[v], kv - NX));
+                a = __dadd_rn(a, -in.xf(xm[v], kv - 1));
+                a = __dadd_rn(a, __dmul_rn(g.diag, in.xf(qc[v], kv)));
+                a = __dadd_rn(a, -in.xf(xp[v], kv + 1));
+                a = __dadd_rn(a, -in.xf(yp[v], kv + NX));
+                a = __dadd_rn(a, -in.xf(qp[v], kv + sxy));
+                n[v] = a;
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < VX; ++v) n[v] = 0.0;
+        }
+        if (ok) body.template compute<VX>(k, cur, n, qc, acc);
+        if constexpr (Body::kStencil) {
+            if (z + 1 < z1) {
+                stage(sp[kb ^ 1], qp, h1);
+                h1 = h2;
+            }
+#pragma unroll
+            for (int v = 0; v < VX; ++v) { qm[v] = qc[v]; qc[v] = qp[v]; qp[v] = qn[v]; }
+        }
+        cur = nxt;
+    }
+
+    if constexpr (Q > 0) {
+        double t[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            t[q] = acc[q][0];
+            if constexpr (VX == 2) t[q] = __dadd_rn(acc[q][0], acc[q][1]);
+        }
+        block_sum<Q>(t, sred);
+        if (tid == 0) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) ws.items[item * NQ + q] = t[q];
+        }
+        complete_item<Q>(ws, cfg, L, phase, c, sred);
+    }
+}
+
+template <class In, class Body>
+__global__ void __launch_bounds__(NT, 2)
+csr_sweep(CGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
+    constexpr int Q = Body::NQ;
+    __shared__ double sprod[Body::kStencil ? CSR_WIN : 1];
+    __shared__ double sred[NQ * NWARP];
+    if (!pred_ok(ws.head, pred, row)) return;
+    body.setup(ws);
+    in.setup(ws);
+
+    const int tid = threadIdx.x;
+    const long long item = blockIdx.x;
+    const long long r0 = item * RB;
+    const long long r = r0 + tid;
+    const bool ok = r < g.n;
+    double n[1] = {0.0};
+    double cen[1] = {0.0};
+    if constexpr (Body::kStencil) {
+        const long long rend = min(r0 + RB, g.n);
+        const long long k0 = g.row_ptr[r0], k1 = g.row_ptr[rend];
+        long long lo = 0, hi = 0;
+        if (ok) { lo = g.row_ptr[r]; hi = g.row_ptr[r + 1]; }
+        double a = 0.0;
+        for (long long wk = k0; wk < k1; wk += CSR_WIN) {
+            const long long we = min(wk + (long long)CSR_WIN, k1);
+            for (long long kk = wk + tid; kk < we; kk += NT) {
+                const int col = __ldcs(g.col_idx + kk);
+                double raw[1];
+                in.template raw<1>(in.base(), col, raw);
+                sprod[kk - wk] = __dmul_rn(__ldcs(g.values + kk), in.xf(raw[0], col));
+            }
+            __syncthreads();
+            const long long a0 = max(lo, wk), a1 = min(hi, we);
+            for (long long kk = a0; kk < a1; ++kk) a = __dadd_rn(a, sprod[kk - wk]);
+            __syncthreads();
+        }
+        n[0] = a;
+        if (ok) in.template raw<1>(in.base(), r, cen);
+    }
+    double acc[Q > 0 ? Q : 1][1];
+#pragma unroll
+    for (int q = 0; q < (Q > 0 ? Q : 1); ++q) acc[q][0] = 0.0;
+    if (ok) {
+        typename Body::template Regs<1> R;
+        body.template load<1>(r, R);
+        body.template compute<1>(r, R, n, cen, acc);
+    }
+    if constexpr (Q > 0) {
+        double t[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) t[q] = acc[q][0];
+        block_sum<Q>(t, sred);
+        if (tid == 0) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) ws.items[item * NQ + q] = t[q];
+        }
+        complete_item<Q>(ws, cfg, L, phase, item / L.T, sred);
+    }
+}
+
+// Tiny single-CTA kernel: level-4 fold of the (gathered) chunk table + epilogue.
+__global__ void __launch_bounds__(NT) finalize_kernel(Ws ws, Cfg cfg, int phase, int pred, long long row) {
+    __shared__ double sred[NQ * NWARP];
+    if (!pred_ok(ws.head, pred, row)) return;
+    double f[NQ];
+    strided_sum<NQ>(ws.chunks, ws.chunks_global, NQ, f, sred);
+    if (threadIdx.x == 0) finalize(ws, cfg, phase, f);
+}
+
+}  // namespace kpl

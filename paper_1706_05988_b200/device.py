@@ -1,0 +1,205 @@
+"""Device residency: operators, preconditioners and vectors in HBM.
+
+* CSR matrices are uploaded once as int32 `row_ptr`/`col_idx` + fp64
+  `values` (the reference stores int64, sparse.py:48-50; every BASELINE
+  config fits int32: nnz <= 2^31-1 is checked) and cached per matrix object.
+* Stencil operators upload nothing.
+* Jacobi uploads `inv_diag` (CSR) or passes the constant fl(1/diag)
+  (stencils), cached per preconditioner object.
+
+All device memory is owned by PyTorch's caching allocator; the C library
+only receives raw pointers.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+
+from . import _lib
+from ._lib import KplError, KplOp
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise KplError("no CUDA device: the p-CG-sh path runs only on the GPU (no CPU fallback)")
+    _lib.load()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_handle():
+    return torch().cuda.current_stream().cuda_stream
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+# Reference SparseMatrix objects use __slots__ without a cache slot; keep a
+# small identity-keyed cache (strong refs, bounded) for those.
+_foreign_cache: dict = {}
+_FOREIGN_MAX = 4
+
+
+class DeviceMatrix:
+    """Device copy of an operator (CSR arrays or stencil geometry)."""
+
+    def __init__(self, A, device):
+        t = torch()
+        self.n = int(A.n)
+        if hasattr(A, "stencil_spec"):
+            self.kind = _lib.KPL_OP_STENCIL
+            self.nx, self.ny, self.nz, self.diag = A.stencil_spec()
+            self.row_ptr = self.col_idx = self.values = None
+            self.nnz = 0
+        else:
+            self.kind = _lib.KPL_OP_CSR
+            nnz = len(A.values)
+            if nnz >= 2**31 or self.n >= 2**31:
+                raise ValueError("matrix too large for int32 CSR indices")
+            self.row_ptr = t.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int32)).to(device)
+            self.col_idx = t.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int32)).to(device)
+            self.values = t.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(device)
+            self.nnz = nnz
+            self.nx = self.ny = self.nz = 0
+            self.diag = 0.0
+
+
+def device_matrix(A, device) -> DeviceMatrix:
+    cached = getattr(A, "_device", None) if _has_slot(A) else None
+    if cached is not None:
+        return cached
+    if not _has_slot(A):
+        hit = _foreign_cache.get(id(A))
+        if hit is not None and hit[0] is A:
+            return hit[1]
+    dm = DeviceMatrix(A, device)
+    if _has_slot(A):
+        A._device = dm
+    else:
+        if len(_foreign_cache) >= _FOREIGN_MAX:
+            _foreign_cache.pop(next(iter(_foreign_cache)))
+        _foreign_cache[id(A)] = (A, dm)
+    return dm
+
+
+def _has_slot(obj):
+    try:
+        getattr(obj, "_device")
+        return True
+    except AttributeError:
+        return False
+
+
+class DevicePrecond:
+    def __init__(self, M, dm: DeviceMatrix, device):
+        t = torch()
+        kind = "identity" if M is None else getattr(M, "kind", "identity")
+        self.inv_diag = None
+        self.const = 0.0
+        if kind == "identity":
+            self.code = _lib.KPL_PC_IDENTITY
+        elif kind == "jacobi":
+            const = getattr(M, "inv_const", None)
+            if const is None and dm.kind == _lib.KPL_OP_STENCIL:
+                inv = np.asarray(M.inv_diag, dtype=np.float64)
+                if not np.all(inv == inv[0]):
+                    raise ValueError("stencil operators need a constant Jacobi diagonal")
+                const = float(inv[0])
+            if dm.kind == _lib.KPL_OP_STENCIL:
+                self.code = _lib.KPL_PC_JACOBI_CONST
+                self.const = float(const)
+            else:
+                self.code = _lib.KPL_PC_JACOBI_VEC
+                inv = M.inv_diag
+                if len(inv) != dm.n:
+                    raise ValueError("dimension mismatch in preconditioner apply")
+                self.inv_diag = t.from_numpy(np.ascontiguousarray(inv, dtype=np.float64)).to(device)
+        else:
+            raise NotImplementedError(
+                f"preconditioner kind {kind!r} is not on the device path (identity/jacobi only)")
+
+    @property
+    def identity(self):
+        return self.code == _lib.KPL_PC_IDENTITY
+
+
+_pc_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def device_precond(M, dm, device) -> DevicePrecond:
+    if M is None or getattr(M, "kind", "identity") == "identity":
+        return DevicePrecond(None, dm, device)
+    key = (id(dm),)
+    try:
+        hit = _pc_cache.get(M)
+    except TypeError:
+        hit = None
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    dp = DevicePrecond(M, dm, device)
+    try:
+        _pc_cache[M] = (key, dp)
+    except TypeError:
+        pass
+    return dp
+
+
+def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk_blocks=0) -> KplOp:
+    op = KplOp()
+    op.kind = dm.kind
+    op.precond = dp.code if dp is not None else _lib.KPL_PC_IDENTITY
+    op.n = dm.n
+    if dm.kind == _lib.KPL_OP_STENCIL:
+        op.nx, op.ny, op.nz, op.diag = dm.nx, dm.ny, dm.nz, float(dm.diag)
+    else:
+        op.row_ptr = ptr(dm.row_ptr)
+        op.col_idx = ptr(dm.col_idx)
+        op.values = ptr(dm.values)
+        op.nnz = dm.nnz
+    op.zc = zc
+    op.vx = vx
+    op.chunk_blocks = chunk_blocks
+    if dp is not None:
+        op.pc_const = dp.const
+        op.inv_diag = ptr(dp.inv_diag)
+    return op
+
+
+def vector_op(n) -> KplOp:
+    """Layout descriptor for plain vectors (dot without an operator)."""
+    op = KplOp()
+    op.kind = _lib.KPL_OP_CSR
+    op.n = n
+    return op
+
+
+def to_device_f64(v, n, device, what):
+    """Upload (or adopt) a length-n fp64 vector.
+
+    Returns (tensor, io) with io = "numpy" (host array in, numpy out),
+    "host" (CPU torch tensor in, e.g. pinned memory: CPU tensor out) or
+    False (CUDA tensor in: result stays on the device)."""
+    t = torch()
+    if isinstance(v, t.Tensor):
+        if v.dim() != 1 or v.numel() != n:
+            raise ValueError(f"{what} dimension mismatch")
+        io = "host" if v.device.type == "cpu" else False
+        return v.to(device=device, dtype=t.float64, non_blocking=True).contiguous(), io
+    a = np.asarray(v, dtype=np.float64)
+    if a.shape != (n,):
+        raise ValueError(f"{what} dimension mismatch")
+    host = t.from_numpy(np.ascontiguousarray(a))
+    return host.to(device, non_blocking=False), "numpy"
