@@ -484,7 +484,12 @@ int kpl_solver_finish(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, 
     kpl_status s;
     if ((rc = kpl_read_status(workspace, &s, stream)) != KPL_OK) return rc;
     if (s.state != KPL_ST_DONE) return KPL_OK;
-    if (s.iter % 10 == 0) return KPL_OK;      // cadence already produced it
+    // the final record always carries ||b - A x|| (solvers.py:233-234, `last`);
+    // the cadence produced it already iff its slot is no longer NaN
+    double have = 0.0;
+    cudaMemcpyAsync(&have, ws.hist + 6 * s.iter + 5, sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("finish");
+    if (!std::isnan(have)) return KPL_OK;
     return true_residual(op, L, v, ws, cfg, s.iter, PRED_ROW, st);
 }
 
