@@ -11,8 +11,13 @@
 #include <atomic>
 #include <algorithm>
 
+#include <cudaTypedefs.h>
+#include <cstdlib>
+#include <mutex>
+
 #include "kpl_bodies.cuh"
 #include "kpl_sweep.cuh"
+#include "kpl_tma.cuh"
 
 using namespace kpl;
 
@@ -159,6 +164,61 @@ int with_pc(const kpl_op *op, F &&f) {
         return f(std::integral_constant<int, KPL_PC_JACOBI_VEC>());
     }
     return fail(KPL_EUNSUPPORTED, "CSR operators take identity or vector Jacobi");
+}
+
+// ------------------------------------------------------------ TMA path
+constexpr int kTmaDepth = 2;
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool tma_available() {
+    std::call_once(g_encode_once, [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        cudaGetLastError();
+        if (g_encode) {
+            cudaFuncSetAttribute(pcg_tma_sweep<kTmaDepth>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)TmaRing<kTmaDepth>::bytes());
+            cudaGetLastError();
+        }
+    });
+    const char *env = std::getenv("KPL_NO_TMA");
+    return g_encode != nullptr && !(env && env[0] == '1');
+}
+
+bool encode_box(CUtensorMap *m, const double *base, const kpl_op *op, unsigned bx, unsigned by) {
+    const cuuint64_t dims[3] = {(cuuint64_t)op->nx, (cuuint64_t)op->ny, (cuuint64_t)op->nz};
+    const cuuint64_t strides[2] = {(cuuint64_t)op->nx * 8, (cuuint64_t)op->nx * op->ny * 8};
+    const cuuint32_t box[3] = {bx, by, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The TMA sweep covers the 3D identity-preconditioned p-CG-sh/p-CG/p-CG-rr
+// iteration (config 3's hot kernel); everything else uses the register sweep.
+bool tma_eligible(const kpl_op *op, const Layout &L) {
+    return op->kind == KPL_OP_STENCIL && op->precond == KPL_PC_IDENTITY && L.vx == 2 && L.wx == 1 &&
+           L.wy == NWARP && !op->halo_lo && !op->halo_hi && op->nx % 2 == 0 && tma_available();
+}
+
+int launch_pcg_tma(const kpl_op *op, const Layout &L, const kpl_vecs *v, const BodyPcgIter<KPL_PC_IDENTITY> &body,
+                   const Ws &ws, const Cfg &cfg, int phase, int pred, cudaStream_t st) {
+    TmaMaps maps;
+    bool ok = encode_box(&maps.w[0], v->w0, op, TMA_WX, TMA_WY) && encode_box(&maps.w[1], v->w1, op, TMA_WX, TMA_WY);
+    const double *streams[5] = {v->x, v->r, v->z, v->s, v->t};
+    for (int s = 0; s < 5 && ok; ++s) ok = encode_box(&maps.s[s], streams[s], op, TMA_TX, TMA_TY);
+    if (!ok) return fail(KPL_ECUDA, "cuTensorMapEncodeTiled failed");
+    SGeo g{op->nx, op->ny, op->nz, op->diag, nullptr, nullptr};
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    pcg_tma_sweep<kTmaDepth><<<(unsigned)L.items, NT + 32, TmaRing<kTmaDepth>::bytes(), st>>>(
+        maps, g, L, body, ws, cfg, phase, pred);
+    return cuda_check("tma sweep launch");
 }
 
 __global__ void head_init_kernel(WsHead *h, double *hist, long long nrows, unsigned int *cnt, long long ncnt) {
@@ -414,8 +474,17 @@ int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v,
             body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = sigma;
             body.want_xi = cfg.method == KPL_M_PCG_RR;
             body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
-            int r2 = launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, ws, cfg, PH_PIPE,
+            int r2;
+            if constexpr (PC == KPL_PC_IDENTITY) {
+                if (tma_eligible(op, L))
+                    r2 = launch_pcg_tma(op, L, v, body, ws, cfg, PH_PIPE, PRED_RUNNING, st);
+                else
+                    r2 = launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, ws, cfg, PH_PIPE,
+                                PRED_RUNNING, 0, st);
+            } else {
+                r2 = launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, ws, cfg, PH_PIPE,
                             PRED_RUNNING, 0, st);
+            }
             if (r2 != KPL_OK || cfg.method != KPL_M_PCG_RR) return r2;
             // explicit replacement, predicated on the device trigger (solvers.py:599-607)
             const double *uu = ident ? v->r : v->u;

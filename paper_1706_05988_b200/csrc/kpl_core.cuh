@@ -140,7 +140,7 @@ __device__ __forceinline__ void block_sum(double (&v)[Q], double *sm /* >= NWARP
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int q = 0; q < Q; ++q) v[q] = warp_sum(v[q]);
-    if (lane == 0) {
+    if (lane == 0 && warp < NWARP) {      // extra (producer) warps never contribute
 #pragma unroll
         for (int q = 0; q < Q; ++q) sm[q * NWARP + warp] = v[q];
     }
@@ -166,7 +166,7 @@ __device__ __forceinline__ void strided_sum(const double *src, long long count, 
                                             double (&v)[Q], double *sm) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) v[q] = 0.0;
-    for (long long j = threadIdx.x; j < count; j += NT) {
+    for (long long j = threadIdx.x; j < count && threadIdx.x < NT; j += NT) {
 #pragma unroll
         for (int q = 0; q < Q; ++q) v[q] = __dadd_rn(v[q], __ldcg(src + j * stride + q));
     }

@@ -254,3 +254,28 @@ def test_device_tensor_io_stays_on_device():
     b = torch.ones(A.n, dtype=torch.float64, device="cuda")
     res = K.solve(A, None, b, None, K.SolverConfig(method="pcg_sh", shift=2.0, max_iters=30))
     assert isinstance(res.x, torch.Tensor) and res.x.is_cuda
+
+
+@pytest.mark.parametrize("shape,zc", [((70, 20, 9), 0), ((64, 64, 48), 16), ((130, 9, 17), 4)])
+def test_stencil3d_shapes_bitwise(shape, zc):
+    """Tile-edge, chunk-edge and partial-chunk geometries of the 3D sweep
+    (TMA-fed on sm_100a) against the oracle with the device order."""
+    A = K.Stencil3D(*shape)
+    b = O.spmv(O.as_oracle_operator(A), np.full(A.n, 1 / math.sqrt(A.n)))
+    cfg = dict(method="pcg_sh", shift=2.30188679245283, max_iters=40, rtol=0.0)
+    from paper_1706_05988_b200.solvers import _Solve
+    S = _Solve(A, None, b, None, K.SolverConfig(**cfg), zc=zc)
+    res = S.run()
+    ores = O.solve(A, None, b, None, O.Config(**cfg), dot=gpu_dot(A, zc=zc))
+    assert same_bits(hist6(res), oracle_hist6(ores)), first_diff(hist6(res), oracle_hist6(ores))
+    assert same_bits(res.x, ores.x)
+
+
+def test_tma_and_register_sweeps_identical(monkeypatch):
+    A = K.Stencil3D(96, 40, 24)
+    b = np.random.default_rng(5).normal(size=A.n)
+    cfg = K.SolverConfig(method="pcg_rr", max_iters=60)
+    r1 = K.solve(A, None, b, None, cfg)
+    monkeypatch.setenv("KPL_NO_TMA", "1")
+    r2 = K.solve(A, None, b, None, cfg)
+    assert same_bits(hist6(r1), hist6(r2)) and same_bits(r1.x, r2.x)
