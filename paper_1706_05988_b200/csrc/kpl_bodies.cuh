@@ -80,6 +80,13 @@ struct InCgP {
     __device__ double xf(double r, long long) const { return r; }
 };
 
+// Shared-memory stream plane accessor for the TMA sweep: stream s of the
+// stage at S + s*512, own pair at offset cs.
+__device__ __forceinline__ void sm2(const double *S, int s, int cs, double (&o)[2]) {
+    const double2 t = *reinterpret_cast<const double2 *>(S + s * 512 + cs);
+    o[0] = t.x; o[1] = t.y;
+}
+
 // ---------------------------------------------------------------- bodies
 // out = A v  (sparse.py:153-160)
 struct BodySpmv {
@@ -127,11 +134,13 @@ struct BodyInitR {
     double c;
     int copy_x;
     template <int V> struct Regs { double b[V], d[V]; };
+    static constexpr int kTmaStreams = 1;                 // b
     __device__ void setup(const Ws &) {}
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
         ld_cs<V>(b, k, R.b);
         if constexpr (PC == KPL_PC_JACOBI_VEC) ld_cs<V>(dinv, k, R.d);
     }
+    __device__ void load_tma(const double *S, int cs, Regs<2> &R) const { sm2(S, 0, cs, R.b); }
     template <int V>
     __device__ void compute(long long k, const Regs<V> &R, const double (&n)[V], const double (&xin)[V],
                             double (&acc)[NQ][V]) const {
@@ -158,8 +167,10 @@ struct BodyTrue {
     static constexpr bool kStencil = true;
     const double *b;
     template <int V> struct Regs { double b[V]; };
+    static constexpr int kTmaStreams = 1;                 // b
     __device__ void setup(const Ws &) {}
     template <int V> __device__ void load(long long k, Regs<V> &R) const { ld_cs<V>(b, k, R.b); }
+    __device__ void load_tma(const double *S, int cs, Regs<2> &R) const { sm2(S, 0, cs, R.b); }
     template <int V>
     __device__ void compute(long long, const Regs<V> &R, const double (&n)[V], const double (&)[V],
                             double (&acc)[1][V]) const {
@@ -181,11 +192,13 @@ struct BodyInitW {
     double sigma;
     int ident;
     template <int V> struct Regs { double r[V], u[V]; };
+    static constexpr int kTmaStreams = 1;                 // r (identity preconditioner: u == r)
     __device__ void setup(const Ws &) {}
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
         ld_cs<V>(r, k, R.r);
         if (!ident) ld_cs<V>(u, k, R.u);
     }
+    __device__ void load_tma(const double *S, int cs, Regs<2> &R) const { sm2(S, 0, cs, R.r); }
     template <int V>
     __device__ void compute(long long k, const Regs<V> &R, const double (&n)[V], const double (&uc)[V],
                             double (&acc)[NQ][V]) const {
@@ -221,6 +234,10 @@ struct BodyPcgIter {
     double alpha, beta, asig;
     double *wout;
     template <int V> struct Regs { double x[V], r[V], z[V], s[V], t[V], u[V], q[V], p[V], d[V]; };
+    static constexpr int kTmaStreams = 5;                 // x, r, z, s, t (identity preconditioner)
+    __device__ void load_tma(const double *S, int cs, Regs<2> &R) const {
+        sm2(S, 0, cs, R.x); sm2(S, 1, cs, R.r); sm2(S, 2, cs, R.z); sm2(S, 3, cs, R.s); sm2(S, 4, cs, R.t);
+    }
     __device__ void setup(const Ws &ws) {
         alpha = ws.head->alpha;
         beta = ws.head->beta;

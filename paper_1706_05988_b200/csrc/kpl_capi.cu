@@ -172,6 +172,13 @@ constexpr int kTmaDepth = 2;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
+template <class Body>
+void tma_prepare() {
+    cudaFuncSetAttribute(tma_sweep<Body, kTmaDepth>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TmaRing<kTmaDepth, Body::kTmaStreams>::bytes());
+    cudaGetLastError();
+}
+
 bool tma_available() {
     std::call_once(g_encode_once, [] {
         void *fn = nullptr;
@@ -181,9 +188,10 @@ bool tma_available() {
             g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
         cudaGetLastError();
         if (g_encode) {
-            cudaFuncSetAttribute(pcg_tma_sweep<kTmaDepth>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)TmaRing<kTmaDepth>::bytes());
-            cudaGetLastError();
+            tma_prepare<BodyPcgIter<KPL_PC_IDENTITY>>();
+            tma_prepare<BodyTrue>();
+            tma_prepare<BodyInitR<KPL_PC_IDENTITY>>();
+            tma_prepare<BodyInitW>();
         }
     });
     const char *env = std::getenv("KPL_NO_TMA");
@@ -200,24 +208,30 @@ bool encode_box(CUtensorMap *m, const double *base, const kpl_op *op, unsigned b
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// The TMA sweep covers the 3D identity-preconditioned p-CG-sh/p-CG/p-CG-rr
-// iteration (config 3's hot kernel); everything else uses the register sweep.
+// TMA sweeps cover the 3D identity-preconditioned stencil sweeps (config 3's
+// hot kernel and its cadence/init sweeps); everything else uses the register
+// sweep of kpl_sweep.cuh.
 bool tma_eligible(const kpl_op *op, const Layout &L) {
     return op->kind == KPL_OP_STENCIL && op->precond == KPL_PC_IDENTITY && L.vx == 2 && L.wx == 1 &&
            L.wy == NWARP && !op->halo_lo && !op->halo_hi && op->nx % 2 == 0 && tma_available();
 }
 
-int launch_pcg_tma(const kpl_op *op, const Layout &L, const kpl_vecs *v, const BodyPcgIter<KPL_PC_IDENTITY> &body,
-                   const Ws &ws, const Cfg &cfg, int phase, int pred, cudaStream_t st) {
+// in0/in1: stencil input (ping-pong pair or twice the same vector, wsel 0/1);
+// streams: the body's kTmaStreams plane-wise operands.
+template <class Body>
+int launch_tma(const kpl_op *op, const Layout &L, const double *in0, const double *in1, int wsel,
+               const double *const *streams, const Body &body, const Ws &ws, const Cfg &cfg, int phase,
+               int pred, long long row, cudaStream_t st) {
+    constexpr int NSTR = Body::kTmaStreams;
     TmaMaps maps;
-    bool ok = encode_box(&maps.w[0], v->w0, op, TMA_WX, TMA_WY) && encode_box(&maps.w[1], v->w1, op, TMA_WX, TMA_WY);
-    const double *streams[5] = {v->x, v->r, v->z, v->s, v->t};
-    for (int s = 0; s < 5 && ok; ++s) ok = encode_box(&maps.s[s], streams[s], op, TMA_TX, TMA_TY);
+    std::memset(&maps, 0, sizeof(maps));
+    bool ok = encode_box(&maps.w[0], in0, op, TMA_WX, TMA_WY) && encode_box(&maps.w[1], in1, op, TMA_WX, TMA_WY);
+    for (int s = 0; s < NSTR && ok; ++s) ok = encode_box(&maps.s[s], streams[s], op, TMA_TX, TMA_TY);
     if (!ok) return fail(KPL_ECUDA, "cuTensorMapEncodeTiled failed");
     SGeo g{op->nx, op->ny, op->nz, op->diag, nullptr, nullptr};
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    pcg_tma_sweep<kTmaDepth><<<(unsigned)L.items, NT + 32, TmaRing<kTmaDepth>::bytes(), st>>>(
-        maps, g, L, body, ws, cfg, phase, pred);
+    tma_sweep<Body, kTmaDepth><<<(unsigned)L.items, NT + 32, TmaRing<kTmaDepth, NSTR>::bytes(), st>>>(
+        maps, g, L, body, ws, cfg, phase, pred, row, wsel);
     return cuda_check("tma sweep launch");
 }
 
@@ -400,6 +414,12 @@ int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, co
         BodyInitR<PC> body;
         body.b = v->b; body.x = v->x; body.r = v->r; body.u = v->u;
         body.dinv = op->inv_diag; body.c = op->pc_const; body.copy_x = copy_x;
+        if constexpr (PC == KPL_PC_IDENTITY) {
+            if (tma_eligible(op, L)) {
+                const double *streams[1] = {v->b};
+                return launch_tma(op, L, xin, xin, 0, streams, body, ws, cfg, PH_INITR, PRED_ALWAYS, 0, st);
+            }
+        }
         return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, xin, xin, SEL_FIXED), body, ws, cfg,
                       PH_INITR, PRED_ALWAYS, 0, st);
     });
@@ -420,6 +440,10 @@ int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, co
     }
     BodyInitW body;
     body.r = v->r; body.u = u; body.w = v->w0; body.sigma = sigma; body.ident = ident;
+    if (ident && tma_eligible(op, L)) {
+        const double *streams[1] = {v->r};
+        return launch_tma(op, L, u, u, 0, streams, body, ws, cfg, PH_PIPE, PRED_ALWAYS, 0, st);
+    }
     return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, u, u, SEL_FIXED), body, ws, cfg, PH_PIPE,
                   PRED_ALWAYS, 0, st);
 }
@@ -429,6 +453,10 @@ static int true_residual(const kpl_op *op, const Layout &L, const kpl_vecs *v, c
                          long long row, int pred, cudaStream_t st) {
     BodyTrue body;
     body.b = v->b;
+    if (tma_eligible(op, L)) {
+        const double *streams[1] = {v->b};
+        return launch_tma(op, L, v->x, v->x, 0, streams, body, ws, cfg, PH_TRUE, pred, row, st);
+    }
     return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), body, ws, cfg, PH_TRUE, pred,
                   row, st);
 }
@@ -476,8 +504,10 @@ int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v,
             body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
             int r2;
             if constexpr (PC == KPL_PC_IDENTITY) {
-                if (tma_eligible(op, L))
-                    r2 = launch_pcg_tma(op, L, v, body, ws, cfg, PH_PIPE, PRED_RUNNING, st);
+                if (tma_eligible(op, L)) {
+                    const double *streams[5] = {v->x, v->r, v->z, v->s, v->t};
+                    r2 = launch_tma(op, L, v->w0, v->w1, 1, streams, body, ws, cfg, PH_PIPE, PRED_RUNNING, 0, st);
+                }
                 else
                     r2 = launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, ws, cfg, PH_PIPE,
                                 PRED_RUNNING, 0, st);

@@ -16,7 +16,8 @@
 // The w ring holds SW = D+3 planes (stencil needs z-1..z+1, D planes ahead);
 // the stream ring SS = D+1 stages.  Dirichlet ghosts (x,y,z out of range) are
 // the TMA out-of-bounds zero fill, so the consumer has no boundary logic.
-// With D = 2: 5 x 5.4 KB + 3 x 20 KB ~ 89 KB smem per CTA, 2 CTAs per SM,
+// With D = 2 and the 5 streams of the p-CG-sh update: 5 x 5.4 KB + 3 x 20 KB
+// ~ 89 KB smem per CTA, 2 CTAs per SM,
 // ~100 KB of loads in flight per SM (vs ~49 KB for the register-prefetch sweep).
 #pragma once
 #include <cuda.h>
@@ -71,33 +72,37 @@ __device__ __forceinline__ void tma_load3d(void *dst, const CUtensorMap *map, in
         : "memory");
 }
 
-template <int D>
+template <int D, int NSTR>
 struct TmaRing {
     static constexpr int SW = D + 3, SS = D + 1;
     static constexpr size_t bytes() {
-        return (size_t)SW * TMA_WPLANE * 8 + (size_t)SS * TMA_NS * TMA_SPLANE * 8 + 8 * 2 * (SW + SS);
+        return (size_t)SW * TMA_WPLANE * 8 + (size_t)SS * NSTR * TMA_SPLANE * 8 + 8 * 2 * (SW + SS);
     }
 };
 
-// PC == IDENTITY only (6 live vectors: streams x, r, z, s, t + the w ring).
-template <int D>
+// Generic over bodies that declare kTmaStreams (<= 5) and load_tma(); the
+// stencil input ring is maps.w[wsel ? iter & 1 : 0].  Identity preconditioner
+// only (the stencil input is used raw).
+template <class Body, int D>
 __global__ void __launch_bounds__(NT + 32, 2)
-pcg_tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, BodyPcgIter<KPL_PC_IDENTITY> body, Ws ws,
-              Cfg cfg, int phase, int pred) {
-    constexpr int SW = TmaRing<D>::SW, SS = TmaRing<D>::SS;
-    constexpr int Q = BodyPcgIter<KPL_PC_IDENTITY>::NQ;
+tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws ws, Cfg cfg, int phase,
+          int pred, long long row, int wsel) {
+    constexpr int NSTR = Body::kTmaStreams;
+    constexpr int SW = TmaRing<D, NSTR>::SW, SS = TmaRing<D, NSTR>::SS;
+    constexpr int Q = Body::NQ > 0 ? Body::NQ : 1;
+    constexpr unsigned SBYTES = NSTR * TMA_SPLANE * 8;
     extern __shared__ __align__(128) unsigned char smem[];
     double *wring = reinterpret_cast<double *>(smem);
     double *sring = wring + SW * TMA_WPLANE;
-    unsigned long long *wfull = reinterpret_cast<unsigned long long *>(sring + SS * TMA_NS * TMA_SPLANE);
+    unsigned long long *wfull = reinterpret_cast<unsigned long long *>(sring + SS * NSTR * TMA_SPLANE);
     unsigned long long *sfull = wfull + SW;
     unsigned long long *wempty = sfull + SS;
     unsigned long long *sempty = wempty + SW;
     __shared__ double sred[NQ * NWARP];
 
-    if (!pred_ok(ws.head, pred, 0)) return;
+    if (!pred_ok(ws.head, pred, row)) return;
     body.setup(ws);
-    const long long par = ws.head->iter & 1;                 // w_in = w[iter & 1]
+    const long long par = wsel ? (ws.head->iter & 1) : 0;    // w_in = w[iter & 1] (ping-pong) or fixed
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long item = blockIdx.x;
@@ -136,10 +141,10 @@ pcg_tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, BodyPcgIte
                 } else {
                     const int slot = q % SS;
                     if (q >= SS) mbar_wait(&sempty[slot], ((q / SS) - 1) & 1);
-                    mbar_expect_tx(&sfull[slot], TMA_SBYTES);
+                    mbar_expect_tx(&sfull[slot], SBYTES);
 #pragma unroll
-                    for (int s = 0; s < TMA_NS; ++s)
-                        tma_load3d(sring + (slot * TMA_NS + s) * TMA_SPLANE, &maps.s[s], x0, y0, z0 + q,
+                    for (int s = 0; s < NSTR; ++s)
+                        tma_load3d(sring + (slot * NSTR + s) * TMA_SPLANE, &maps.s[s], x0, y0, z0 + q,
                                    &sfull[slot]);
                     ++q;
                 }
@@ -164,7 +169,7 @@ pcg_tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, BodyPcgIte
             const double *Wm = wring + (k % SW) * TMA_WPLANE;
             const double *Wc = wring + ((k + 1) % SW) * TMA_WPLANE;
             const double *Wp = wring + (pz % SW) * TMA_WPLANE;
-            const double *Sp = sring + (k % SS) * TMA_NS * TMA_SPLANE;
+            const double *Sp = sring + (k % SS) * NSTR * TMA_SPLANE;
             if (ok) {
                 const double2 qm = *reinterpret_cast<const double2 *>(Wm + cw);
                 const double2 qc = *reinterpret_cast<const double2 *>(Wc + cw);
@@ -172,16 +177,8 @@ pcg_tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, BodyPcgIte
                 const double2 ym = *reinterpret_cast<const double2 *>(Wc + cw - TMA_WX);
                 const double2 yp = *reinterpret_cast<const double2 *>(Wc + cw + TMA_WX);
                 const double xm0 = Wc[cw - 1], xp1 = Wc[cw + 2];
-                typename BodyPcgIter<KPL_PC_IDENTITY>::template Regs<2> R;
-                {
-                    const double2 a = *reinterpret_cast<const double2 *>(Sp + 0 * TMA_SPLANE + cs);
-                    const double2 b = *reinterpret_cast<const double2 *>(Sp + 1 * TMA_SPLANE + cs);
-                    const double2 cz = *reinterpret_cast<const double2 *>(Sp + 2 * TMA_SPLANE + cs);
-                    const double2 d = *reinterpret_cast<const double2 *>(Sp + 3 * TMA_SPLANE + cs);
-                    const double2 e = *reinterpret_cast<const double2 *>(Sp + 4 * TMA_SPLANE + cs);
-                    R.x[0] = a.x; R.x[1] = a.y; R.r[0] = b.x; R.r[1] = b.y; R.z[0] = cz.x; R.z[1] = cz.y;
-                    R.s[0] = d.x; R.s[1] = d.y; R.t[0] = e.x; R.t[1] = e.y;
-                }
+                typename Body::template Regs<2> R;
+                body.load_tma(Sp, cs, R);
                 // 7-point stencil, terms in ascending column order (as csr_matvec)
                 const double zmv[2] = {qm.x, qm.y}, ymv[2] = {ym.x, ym.y}, xmv[2] = {xm0, qc.x};
                 const double cv[2] = {qc.x, qc.y}, xpv[2] = {qc.y, xp1}, ypv[2] = {yp.x, yp.y},
@@ -210,15 +207,17 @@ pcg_tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, BodyPcgIte
         }
     }
 
-    double t[Q];
+    if constexpr (Body::NQ > 0) {
+        double t[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) t[q] = __dadd_rn(acc[q][0], acc[q][1]);
-    block_sum<Q>(t, sred);
-    if (tid == 0) {
+        for (int q = 0; q < Q; ++q) t[q] = __dadd_rn(acc[q][0], acc[q][1]);
+        block_sum<Q>(t, sred);
+        if (tid == 0) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q) ws.items[item * NQ + q] = t[q];
+            for (int q = 0; q < Q; ++q) ws.items[item * NQ + q] = t[q];
+        }
+        complete_item<Q>(ws, cfg, L, phase, c, sred);
     }
-    complete_item<Q>(ws, cfg, L, phase, c, sred);
 }
 
 }  // namespace kpl
