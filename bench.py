@@ -250,7 +250,7 @@ def run_ours(args):
             "unit": "GB/s",
             "frac": achieved / peak,
             "traffic": traffic,
-            "kernel": "stencil_sweep<2, InVec<0>, BodyPcgIter<0>> (fused SpMV + 9 recurrences + dots)",
+            "kernel": "tma_sweep<BodyPcgIter<0>, 2> (TMA-fed fused 7-point SpMV + 9 recurrences + next dots)",
             "algorithmic_bytes_per_launch": alg_bytes,
             "launch_ms": t_kernel * 1000.0,
             "peak_kind": peak_kind,

@@ -153,7 +153,10 @@ class _Solve:
         c.rr_threshold = float(cfg.rr_threshold)
         if cfg.method == "pcg_rr":
             # _ReplacementTrigger.coef = (mu*sqrt(n) + 1) * ||A||_inf (solvers.py:514)
-            c.rr_coef = (A.mu * math.sqrt(A.n) + 1.0) * A.norm_inf()
+            dm = self.dm
+            if getattr(dm, "rr_coef", None) is None:
+                dm.rr_coef = (A.mu * math.sqrt(A.n) + 1.0) * A.norm_inf()
+            c.rr_coef = dm.rr_coef
         self.kcfg = c
         ident = self.dp.identity
         f64 = dict(dtype=t.float64, device=dev)
