@@ -64,7 +64,9 @@ typedef struct kpl_op {
     const double  *values;
     int64_t nnz;
     int32_t chunk_blocks;    /* 256-row blocks per reduction chunk (0 = default) */
-    int32_t _pad0;
+    int32_t zhalo;           /* stencil: 1 = every stencil-input vector carries one
+                                halo plane before plane 0 and after plane nz-1
+                                (z-slab multi-GPU; filled by the caller)       */
     /* preconditioner                                                        */
     double  pc_const;        /* KPL_PC_JACOBI_CONST                              */
     const double *inv_diag;  /* KPL_PC_JACOBI_VEC, length n (gathered via col)   */
@@ -174,13 +176,35 @@ int kpl_solver_finish(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
 /* Synchronous copy of the device status to host memory `out`.               */
 int kpl_read_status(const void *workspace, kpl_status *out, void *stream);
 
+/* ---- sweep-level interface (multi-GPU drivers, custom schedules) ------- */
+#define KPL_SW_BNORM   1   /* ||b|| (solvers.py:372)                              */
+#define KPL_SW_INIT_R  2   /* r = b - A x, u = M r (input x) (:374-375)           */
+#define KPL_SW_INIT_W  3   /* w = A u - sigma r + row-0 reductions (:376, :388)   */
+#define KPL_SW_ITER    4   /* fused pipelined iteration (:408-421 + :388-390)      */
+#define KPL_SW_TRUE    5   /* ||b - A x|| into history row `row` (:233-234)       */
+#define KPL_SW_CG_P    6   /* classic CG p, s = A p, delta (:269-289)             */
+#define KPL_SW_CG_X    7   /* classic CG x, r, u + next head (:290-292, :258)     */
+#define KPL_SW_RR_R    8   /* replacement r = b - A x, u = M r (:600-601)         */
+#define KPL_SW_RR_W    9   /* replacement w = A u (:602)                          */
+#define KPL_SW_RR_S   10   /* replacement s = A p, q = M s (:603-604)             */
+#define KPL_SW_RR_Z   11   /* replacement z = A q + next reductions (:605)        */
+/* Reset the workspace head/history and zero the state vectors that start at 0. */
+int kpl_solver_prepare(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, void *workspace,
+                       void *stream);
+/* Launch one sweep.  Single GPU (chunks_global == 0): its last CTA folds the
+   reduction and runs the scalar epilogue.  Multi-GPU: it only writes this
+   rank's chunk partials; gather the chunk table, then kpl_finalize_global. */
+int kpl_sweep(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, int32_t kind, int64_t row,
+              void *workspace, void *stream);
+/* Reduction phase of a sweep kind (0 = no reduction / nothing to finalize). */
+int kpl_sweep_phase(int32_t kind);
+
 /* ---- multi-GPU hooks (one process per GPU; host drives NCCL) ----------- */
-/* Level-4 reduction + scalar update after the chunk partials of all ranks
-   have been gathered into the workspace's global chunk table.  `phase`
-   names the sweep whose partials are pending (returned by
-   kpl_pending_phase).                                                      */
-int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfg, void *workspace,
-                        void *stream);
+/* Level-4 fold of the gathered chunk table + the scalar epilogue of sweep
+   `kind` (same predicate as the sweep).  Every rank runs it on identical
+   data, so every rank holds identical scalars and history.                */
+int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfg, int32_t kind, int64_t row,
+                        void *workspace, void *stream);
 /* Device pointer + byte size of this rank's slice of the chunk table and of
    the whole table (for ncclAllGather).                                      */
 int kpl_chunk_table(const kpl_op *op, void *workspace, void **local, void **global,

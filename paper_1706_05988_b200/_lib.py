@@ -22,6 +22,8 @@ KPL_PC_IDENTITY, KPL_PC_JACOBI_CONST, KPL_PC_JACOBI_VEC = 0, 1, 2
 KPL_M_CG, KPL_M_PCG, KPL_M_PCG_SH, KPL_M_PCG_RR = 0, 1, 2, 4
 KPL_ST_RUNNING, KPL_ST_DONE, KPL_ST_BREAKDOWN = 0, 1, 2
 KPL_HIST_COLS = 6
+(KPL_SW_BNORM, KPL_SW_INIT_R, KPL_SW_INIT_W, KPL_SW_ITER, KPL_SW_TRUE, KPL_SW_CG_P, KPL_SW_CG_X,
+ KPL_SW_RR_R, KPL_SW_RR_W, KPL_SW_RR_S, KPL_SW_RR_Z) = range(1, 12)
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -34,7 +36,7 @@ class KplOp(ctypes.Structure):
                 ("nx", _i64), ("ny", _i64), ("nz", _i64), ("diag", _d),
                 ("zc", _i32), ("vx", _i32), ("halo_lo", _p), ("halo_hi", _p),
                 ("row_ptr", _p), ("col_idx", _p), ("values", _p), ("nnz", _i64),
-                ("chunk_blocks", _i32), ("_pad0", _i32), ("pc_const", _d), ("inv_diag", _p),
+                ("chunk_blocks", _i32), ("zhalo", _i32), ("pc_const", _d), ("inv_diag", _p),
                 ("chunk_offset", _i64), ("chunks_global", _i64)]
 
 
@@ -74,7 +76,12 @@ _SIGS = {
     "kpl_solver_finish": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
                                  ctypes.POINTER(KplVecs), _p, _p]),
     "kpl_read_status": (_i32, [_p, ctypes.POINTER(KplStatus), _p]),
-    "kpl_finalize_global": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), _p, _p]),
+    "kpl_finalize_global": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), _i32, _i64, _p, _p]),
+    "kpl_solver_prepare": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
+                                  ctypes.POINTER(KplVecs), _p, _p]),
+    "kpl_sweep": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), ctypes.POINTER(KplVecs),
+                         _i32, _i64, _p, _p]),
+    "kpl_sweep_phase": (_i32, [_i32]),
     "kpl_chunk_table": (_i32, [ctypes.POINTER(KplOp), _p, ctypes.POINTER(_p), ctypes.POINTER(_p),
                                ctypes.POINTER(_i64)]),
 }

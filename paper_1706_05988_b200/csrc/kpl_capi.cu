@@ -131,7 +131,7 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
     if (L.items <= 0) return KPL_OK;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (op->kind == KPL_OP_STENCIL) {
-        SGeo g{op->nx, op->ny, op->nz, op->diag, op->halo_lo, op->halo_hi};
+        SGeo g{op->nx, op->ny, op->nz, op->diag, op->halo_lo, op->halo_hi, op->zhalo};
         if (L.vx == 2)
             stencil_sweep<2, In, Body><<<(unsigned)L.items, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
         else
@@ -198,8 +198,10 @@ bool tma_available() {
     return g_encode != nullptr && !(env && env[0] == '1');
 }
 
-bool encode_box(CUtensorMap *m, const double *base, const kpl_op *op, unsigned bx, unsigned by) {
-    const cuuint64_t dims[3] = {(cuuint64_t)op->nx, (cuuint64_t)op->ny, (cuuint64_t)op->nz};
+bool encode_box(CUtensorMap *m, const double *base, const kpl_op *op, unsigned bx, unsigned by, int zext = 0) {
+    // zext = 1: the map starts one plane before `base` and spans nz + 2 planes (z halos)
+    base -= zext * op->nx * op->ny;
+    const cuuint64_t dims[3] = {(cuuint64_t)op->nx, (cuuint64_t)op->ny, (cuuint64_t)(op->nz + 2 * zext)};
     const cuuint64_t strides[2] = {(cuuint64_t)op->nx * 8, (cuuint64_t)op->nx * op->ny * 8};
     const cuuint32_t box[3] = {bx, by, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
@@ -214,6 +216,7 @@ bool encode_box(CUtensorMap *m, const double *base, const kpl_op *op, unsigned b
 bool tma_eligible(const kpl_op *op, const Layout &L) {
     return op->kind == KPL_OP_STENCIL && op->precond == KPL_PC_IDENTITY && L.vx == 2 && L.wx == 1 &&
            L.wy == NWARP && !op->halo_lo && !op->halo_hi && op->nx % 2 == 0 && tma_available();
+    // (op->zhalo is supported: the stencil-input maps then cover planes -1..nz)
 }
 
 // in0/in1: stencil input (ping-pong pair or twice the same vector, wsel 0/1);
@@ -225,13 +228,15 @@ int launch_tma(const kpl_op *op, const Layout &L, const double *in0, const doubl
     constexpr int NSTR = Body::kTmaStreams;
     TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
-    bool ok = encode_box(&maps.w[0], in0, op, TMA_WX, TMA_WY) && encode_box(&maps.w[1], in1, op, TMA_WX, TMA_WY);
+    const int zext = op->zhalo ? 1 : 0;
+    bool ok = encode_box(&maps.w[0], in0, op, TMA_WX, TMA_WY, zext) &&
+              encode_box(&maps.w[1], in1, op, TMA_WX, TMA_WY, zext);
     for (int s = 0; s < NSTR && ok; ++s) ok = encode_box(&maps.s[s], streams[s], op, TMA_TX, TMA_TY);
     if (!ok) return fail(KPL_ECUDA, "cuTensorMapEncodeTiled failed");
-    SGeo g{op->nx, op->ny, op->nz, op->diag, nullptr, nullptr};
+    SGeo g{op->nx, op->ny, op->nz, op->diag, nullptr, nullptr, op->zhalo};
     g_launches.fetch_add(1, std::memory_order_relaxed);
     tma_sweep<Body, kTmaDepth><<<(unsigned)L.items, NT + 32, TmaRing<kTmaDepth, NSTR>::bytes(), st>>>(
-        maps, g, L, body, ws, cfg, phase, pred, row, wsel);
+        maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext);
     return cuda_check("tma sweep launch");
 }
 
@@ -375,226 +380,292 @@ int kpl_read_status(const void *workspace, kpl_status *out, void *stream) {
     return KPL_OK;
 }
 
-int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, const double *x0,
-                    void *workspace, void *stream) {
+}  // extern "C"
+
+namespace {
+
+struct Ctx {
+    const kpl_op *op;
     Layout L;
-    int rc = make_layout(op, L);
+    Cfg cfg;
+    Ws ws;
+    const kpl_vecs *v;
+    cudaStream_t st;
+    bool ident;
+    double sigma;
+};
+
+int make_ctx(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, void *workspace, void *stream, Ctx &c) {
+    int rc = make_layout(op, c.L);
     if (rc != KPL_OK) return rc;
     if (!cfgp || !v || !workspace) return fail(KPL_EINVAL, "null argument");
     if ((rc = need_matrix(op)) != KPL_OK) return rc;
-    cudaStream_t st = (cudaStream_t)stream;
-    const Cfg cfg = make_cfg(cfgp);
-    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
-    const long long n = op->n;
-    const bool ident = op->precond == KPL_PC_IDENTITY;
-    const double sigma = cfg.method == KPL_M_PCG_SH ? cfg.shift : 0.0;
+    c.op = op;
+    c.cfg = make_cfg(cfgp);
+    c.ws = make_ws(op, c.L, c.cfg.max_iters, workspace);
+    c.v = v;
+    c.st = (cudaStream_t)stream;
+    c.ident = op->precond == KPL_PC_IDENTITY;
+    c.sigma = c.cfg.method == KPL_M_PCG_SH ? c.cfg.shift : 0.0;
+    return KPL_OK;
+}
 
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    head_init_kernel<<<64, 256, 0, st>>>(ws.head, ws.hist, cfg.max_iters + 1, ws.chunk_cnt, L.nch);
-    if ((rc = cuda_check("head init")) != KPL_OK) return rc;
+// (phase, predicate) of each sweep kind
+int kind_phase(int kind, int &phase, int &pred) {
+    switch (kind) {
+    case KPL_SW_BNORM: phase = PH_BNORM; pred = PRED_ALWAYS; return KPL_OK;
+    case KPL_SW_INIT_R: phase = PH_INITR; pred = PRED_ALWAYS; return KPL_OK;
+    case KPL_SW_INIT_W: phase = PH_PIPE; pred = PRED_ALWAYS; return KPL_OK;
+    case KPL_SW_ITER: phase = PH_PIPE; pred = PRED_RUNNING; return KPL_OK;
+    case KPL_SW_TRUE: phase = PH_TRUE; pred = PRED_ROW; return KPL_OK;
+    case KPL_SW_CG_P: phase = PH_CGDELTA; pred = PRED_RUNNING; return KPL_OK;
+    case KPL_SW_CG_X: phase = PH_CGHEAD; pred = PRED_RUNNING; return KPL_OK;
+    case KPL_SW_RR_R: phase = PH_NONE; pred = PRED_FIRE; return KPL_OK;
+    case KPL_SW_RR_W: phase = PH_NONE; pred = PRED_FIRE; return KPL_OK;
+    case KPL_SW_RR_S: phase = PH_NONE; pred = PRED_FIRE; return KPL_OK;
+    case KPL_SW_RR_Z: phase = PH_RRFINAL; pred = PRED_FIRE; return KPL_OK;
+    default: return fail(KPL_EINVAL, "unknown sweep kind");
+    }
+}
 
-    // bnorm = norm2(b)  (solvers.py:372)
-    {
+// One sweep of the given kind (the building block of every solver sequence).
+// Input vectors of stencil sweeps are read raw at neighbours; with op->zhalo
+// they carry one halo plane on each side (multi-GPU z-slabs).
+int do_sweep(const Ctx &c, int kind, long long row) {
+    const kpl_op *op = c.op;
+    const Layout &L = c.L;
+    const kpl_vecs *v = c.v;
+    int phase, pred;
+    int rc = kind_phase(kind, phase, pred);
+    if (rc != KPL_OK) return rc;
+    const bool tma = tma_eligible(op, L);
+    const double *u = c.ident ? v->r : v->u;
+    switch (kind) {
+    case KPL_SW_BNORM: {                 // norm2(b)  (solvers.py:372)
         BodyDot body;
         body.a = v->b; body.b = v->b;
-        if ((rc = launch(op, L, InNone(), body, ws, cfg, PH_BNORM, PRED_ALWAYS, 0, st)) != KPL_OK) return rc;
+        return launch(op, L, InNone(), body, c.ws, c.cfg, phase, pred, row, c.st);
     }
-    // x = x0.copy(); r = b - A x; u = M r   (solvers.py:373-375)
-    const double *xin = x0;
-    int copy_x = 1;
-    if (!x0) {
-        cudaMemsetAsync(v->x, 0, sizeof(double) * n, st);
-        xin = v->x;
-        copy_x = 0;
-    } else if (x0 == v->x) {
-        copy_x = 0;
-    }
-    rc = with_pc(op, [&](auto pc) -> int {
-        constexpr int PC = decltype(pc)::value;
-        BodyInitR<PC> body;
-        body.b = v->b; body.x = v->x; body.r = v->r; body.u = v->u;
-        body.dinv = op->inv_diag; body.c = op->pc_const; body.copy_x = copy_x;
-        if constexpr (PC == KPL_PC_IDENTITY) {
-            if (tma_eligible(op, L)) {
-                const double *streams[1] = {v->b};
-                return launch_tma(op, L, xin, xin, 0, streams, body, ws, cfg, PH_INITR, PRED_ALWAYS, 0, st);
+    case KPL_SW_INIT_R:                  // r = b - A x; u = M r  (solvers.py:374-375)
+    case KPL_SW_RR_R:                    // replacement r = b - A x, u = M r (:600-601)
+        return with_pc(op, [&](auto pc) -> int {
+            constexpr int PC = decltype(pc)::value;
+            BodyInitR<PC> body;
+            body.b = v->b; body.x = v->x; body.r = v->r; body.u = v->u;
+            body.dinv = op->inv_diag; body.c = op->pc_const; body.copy_x = 0;
+            if constexpr (PC == KPL_PC_IDENTITY) {
+                if (tma) {
+                    const double *streams[1] = {v->b};
+                    return launch_tma(op, L, v->x, v->x, 0, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
+                }
             }
+            return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), body, c.ws, c.cfg, phase,
+                          pred, row, c.st);
+        });
+    case KPL_SW_INIT_W: {                // w = axpy(-sigma, r, A u) + first reductions (:376, :388-390)
+        BodyInitW body;
+        body.r = v->r; body.u = u; body.w = v->w0; body.sigma = c.sigma; body.ident = c.ident;
+        if (c.ident && tma) {
+            const double *streams[1] = {v->r};
+            return launch_tma(op, L, u, u, 0, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
         }
-        return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, xin, xin, SEL_FIXED), body, ws, cfg,
-                      PH_INITR, PRED_ALWAYS, 0, st);
-    });
-    if (rc != KPL_OK) return rc;
-    const double *u = ident ? v->r : v->u;
-
-    if (cfg.method == KPL_M_CG) {
-        cudaMemsetAsync(v->p, 0, sizeof(double) * n, st);      // p = zeros (solvers.py:252)
-        return cuda_check("cg init");
+        return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, u, u, SEL_FIXED), body, c.ws, c.cfg, phase, pred, row,
+                      c.st);
     }
-    // z = q = s = t = p = 0 (solvers.py:377-381); w = axpy(-sigma, r, A u) (:376)
-    cudaMemsetAsync(v->z, 0, sizeof(double) * n, st);
-    cudaMemsetAsync(v->s, 0, sizeof(double) * n, st);
-    cudaMemsetAsync(v->t, 0, sizeof(double) * n, st);
-    if (!ident) {
-        cudaMemsetAsync(v->q, 0, sizeof(double) * n, st);
-        cudaMemsetAsync(v->p, 0, sizeof(double) * n, st);
-    }
-    BodyInitW body;
-    body.r = v->r; body.u = u; body.w = v->w0; body.sigma = sigma; body.ident = ident;
-    if (ident && tma_eligible(op, L)) {
-        const double *streams[1] = {v->r};
-        return launch_tma(op, L, u, u, 0, streams, body, ws, cfg, PH_PIPE, PRED_ALWAYS, 0, st);
-    }
-    return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, u, u, SEL_FIXED), body, ws, cfg, PH_PIPE,
-                  PRED_ALWAYS, 0, st);
-}
-
-// One true-residual sweep for history row `row` (predicated on iter == row).
-static int true_residual(const kpl_op *op, const Layout &L, const kpl_vecs *v, const Ws &ws, const Cfg &cfg,
-                         long long row, int pred, cudaStream_t st) {
-    BodyTrue body;
-    body.b = v->b;
-    if (tma_eligible(op, L)) {
-        const double *streams[1] = {v->b};
-        return launch_tma(op, L, v->x, v->x, 0, streams, body, ws, cfg, PH_TRUE, pred, row, st);
-    }
-    return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), body, ws, cfg, PH_TRUE, pred,
-                  row, st);
-}
-
-int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t first,
-                       int64_t count, void *workspace, void *stream) {
-    Layout L;
-    int rc = make_layout(op, L);
-    if (rc != KPL_OK) return rc;
-    if (!cfgp || !v || !workspace) return fail(KPL_EINVAL, "null argument");
-    cudaStream_t st = (cudaStream_t)stream;
-    const Cfg cfg = make_cfg(cfgp);
-    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
-    const bool ident = op->precond == KPL_PC_IDENTITY;
-    const double sigma = cfg.method == KPL_M_PCG_SH ? cfg.shift : 0.0;
-
-    for (int64_t j = first; j < first + count; ++j) {
-        if (j % 10 == 0) {
-            if ((rc = true_residual(op, L, v, ws, cfg, j, PRED_ROW, st)) != KPL_OK) return rc;
+    case KPL_SW_TRUE: {                  // ||b - A x|| (:233-234, :401-402)
+        BodyTrue body;
+        body.b = v->b;
+        if (tma) {
+            const double *streams[1] = {v->b};
+            return launch_tma(op, L, v->x, v->x, 0, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
         }
-        if (cfg.method == KPL_M_CG) {
-            rc = with_pc(op, [&](auto pc) -> int {
-                constexpr int PC = decltype(pc)::value;
-                InCgP in;
-                in.p0 = v->p; in.p1 = v->p1; in.u = ident ? v->r : v->u; in.p = v->p; in.beta = 0.0;
-                BodyCgP bp;
-                bp.p0 = v->p; bp.p1 = v->p1; bp.s = v->s; bp.pout = v->p1;
-                int r2 = launch(op, L, in, bp, ws, cfg, PH_CGDELTA, PRED_RUNNING, 0, st);
-                if (r2 != KPL_OK) return r2;
-                BodyCgX<PC> bx;
-                bx.x = v->x; bx.r = v->r; bx.u = v->u; bx.p0 = v->p; bx.p1 = v->p1; bx.s = v->s;
-                bx.dinv = op->inv_diag; bx.c = op->pc_const; bx.alpha = 0.0; bx.p = v->p;
-                return launch(op, L, InNone(), bx, ws, cfg, PH_CGHEAD, PRED_RUNNING, 0, st);
-            });
-            if (rc != KPL_OK) return rc;
-            continue;
-        }
-        rc = with_pc(op, [&](auto pc) -> int {
+        return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), body, c.ws, c.cfg, phase, pred,
+                      row, c.st);
+    }
+    case KPL_SW_ITER:                    // the fused pipelined iteration (:408-421 + :388-390)
+        return with_pc(op, [&](auto pc) -> int {
             constexpr int PC = decltype(pc)::value;
             BodyPcgIter<PC> body;
             body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
             body.s = v->s; body.t = v->t; body.p = v->p; body.w0 = v->w0; body.w1 = v->w1;
-            body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = sigma;
-            body.want_xi = cfg.method == KPL_M_PCG_RR;
+            body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = c.sigma;
+            body.want_xi = c.cfg.method == KPL_M_PCG_RR;
             body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
-            int r2;
             if constexpr (PC == KPL_PC_IDENTITY) {
-                if (tma_eligible(op, L)) {
+                if (tma) {
                     const double *streams[5] = {v->x, v->r, v->z, v->s, v->t};
-                    r2 = launch_tma(op, L, v->w0, v->w1, 1, streams, body, ws, cfg, PH_PIPE, PRED_RUNNING, 0, st);
+                    return launch_tma(op, L, v->w0, v->w1, 1, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
                 }
-                else
-                    r2 = launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, ws, cfg, PH_PIPE,
-                                PRED_RUNNING, 0, st);
-            } else {
-                r2 = launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, ws, cfg, PH_PIPE,
-                            PRED_RUNNING, 0, st);
             }
-            if (r2 != KPL_OK || cfg.method != KPL_M_PCG_RR) return r2;
-            // explicit replacement, predicated on the device trigger (solvers.py:599-607)
-            const double *uu = ident ? v->r : v->u;
-            BodyInitR<PC> r1;
-            r1.b = v->b; r1.x = v->x; r1.r = v->r; r1.u = v->u; r1.dinv = op->inv_diag;
-            r1.c = op->pc_const; r1.copy_x = 0;
-            if ((r2 = launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), r1, ws, cfg, PH_NONE,
-                             PRED_FIRE, 0, st)) != KPL_OK) return r2;
-            BodyRepl<PC> rw;
-            rw.mode = 0; rw.w0 = v->w0; rw.w1 = v->w1; rw.s = v->s; rw.q = v->q; rw.dinv = op->inv_diag;
-            rw.c = op->pc_const; rw.wout = v->w1;
-            if ((r2 = launch(op, L, in_vec<KPL_PC_IDENTITY>(op, uu, uu, SEL_FIXED), rw, ws, cfg, PH_NONE,
-                             PRED_FIRE, 0, st)) != KPL_OK) return r2;
-            BodyRepl<PC> rs = rw;
-            rs.mode = 1;
-            const double *pp = ident ? v->t : v->p;
-            if ((r2 = launch(op, L, in_vec<KPL_PC_IDENTITY>(op, pp, pp, SEL_FIXED), rs, ws, cfg, PH_NONE,
-                             PRED_FIRE, 0, st)) != KPL_OK) return r2;
-            BodyReplZ rz;
-            rz.z = v->z; rz.r = v->r; rz.u = uu; rz.w0 = v->w0; rz.w1 = v->w1; rz.ident = ident; rz.w = v->w0;
-            const double *qq = ident ? v->s : v->q;
-            return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, qq, qq, SEL_FIXED), rz, ws, cfg, PH_RRFINAL,
-                          PRED_FIRE, 0, st);
+            return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred, row,
+                          c.st);
         });
-        if (rc != KPL_OK) return rc;
+    case KPL_SW_CG_P: {                  // p = axpy(beta, p, u); s = A p; delta = (s, p) (:269-271)
+        InCgP in;
+        in.p0 = v->p; in.p1 = v->p1; in.u = u; in.p = v->p; in.beta = 0.0;
+        BodyCgP bp;
+        bp.p0 = v->p; bp.p1 = v->p1; bp.s = v->s; bp.pout = v->p1;
+        return launch(op, L, in, bp, c.ws, c.cfg, phase, pred, row, c.st);
+    }
+    case KPL_SW_CG_X:                    // x, r, u updates + next head (:290-292, :258-259)
+        return with_pc(op, [&](auto pc) -> int {
+            constexpr int PC = decltype(pc)::value;
+            BodyCgX<PC> bx;
+            bx.x = v->x; bx.r = v->r; bx.u = v->u; bx.p0 = v->p; bx.p1 = v->p1; bx.s = v->s;
+            bx.dinv = op->inv_diag; bx.c = op->pc_const; bx.alpha = 0.0; bx.p = v->p;
+            return launch(op, L, InNone(), bx, c.ws, c.cfg, phase, pred, row, c.st);
+        });
+    case KPL_SW_RR_W:                    // replacement w = A u (:602)
+    case KPL_SW_RR_S:                    // replacement s = A p, q = M s (:603-604)
+        return with_pc(op, [&](auto pc) -> int {
+            constexpr int PC = decltype(pc)::value;
+            BodyRepl<PC> rw;
+            rw.mode = kind == KPL_SW_RR_W ? 0 : 1;
+            rw.w0 = v->w0; rw.w1 = v->w1; rw.s = v->s; rw.q = v->q; rw.dinv = op->inv_diag;
+            rw.c = op->pc_const; rw.wout = v->w1;
+            const double *in = kind == KPL_SW_RR_W ? u : (c.ident ? v->t : v->p);
+            return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, in, in, SEL_FIXED), rw, c.ws, c.cfg, phase, pred,
+                          row, c.st);
+        });
+    case KPL_SW_RR_Z: {                  // replacement z = A q + the next record's reductions (:605)
+        BodyReplZ rz;
+        rz.z = v->z; rz.r = v->r; rz.u = u; rz.w0 = v->w0; rz.w1 = v->w1; rz.ident = c.ident; rz.w = v->w0;
+        const double *qq = c.ident ? v->s : v->q;
+        return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, qq, qq, SEL_FIXED), rz, c.ws, c.cfg, phase, pred, row,
+                      c.st);
+    }
+    default:
+        return fail(KPL_EINVAL, "unknown sweep kind");
+    }
+}
+
+int head_init(const Ctx &c) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    head_init_kernel<<<64, 256, 0, c.st>>>(c.ws.head, c.ws.hist, c.cfg.max_iters + 1, c.ws.chunk_cnt, c.L.nch);
+    return cuda_check("head init");
+}
+
+// zero the interior of a state vector (halo planes, if any, are the caller's)
+void zero_vec(const Ctx &c, double *p) { cudaMemsetAsync(p, 0, sizeof(double) * c.op->n, c.st); }
+
+}  // namespace
+
+extern "C" {
+
+int kpl_solver_prepare(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, void *workspace, void *stream) {
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
+    if (rc != KPL_OK) return rc;
+    if ((rc = head_init(c)) != KPL_OK) return rc;
+    // state vectors that start at zero (solvers.py:252, :377-381)
+    if (c.cfg.method == KPL_M_CG) {
+        zero_vec(c, v->p);
+    } else {
+        zero_vec(c, v->z);
+        zero_vec(c, v->s);
+        zero_vec(c, v->t);
+        if (!c.ident) { zero_vec(c, v->q); zero_vec(c, v->p); }
+    }
+    return cuda_check("prepare");
+}
+
+int kpl_sweep(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int32_t kind, int64_t row,
+              void *workspace, void *stream) {
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
+    if (rc != KPL_OK) return rc;
+    return do_sweep(c, kind, row);
+}
+
+int kpl_sweep_phase(int32_t kind) {
+    int phase, pred;
+    if (kind_phase(kind, phase, pred) != KPL_OK) return KPL_EINVAL;
+    return phase;
+}
+
+int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, const double *x0,
+                    void *workspace, void *stream) {
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
+    if (rc != KPL_OK) return rc;
+    if (op->chunks_global > 0) return fail(KPL_EINVAL, "multi-GPU operators are driven sweep by sweep");
+    if ((rc = kpl_solver_prepare(op, cfgp, v, workspace, stream)) != KPL_OK) return rc;
+    if ((rc = do_sweep(c, KPL_SW_BNORM, 0)) != KPL_OK) return rc;
+    // x = x0.copy() (solvers.py:373); x0 = None -> zeros
+    if (!x0) cudaMemsetAsync(v->x, 0, sizeof(double) * op->n, c.st);
+    else if (x0 != v->x) cudaMemcpyAsync(v->x, x0, sizeof(double) * op->n, cudaMemcpyDeviceToDevice, c.st);
+    if ((rc = do_sweep(c, KPL_SW_INIT_R, 0)) != KPL_OK) return rc;
+    if (c.cfg.method == KPL_M_CG) return KPL_OK;           // head of row 0 done by INIT_R's epilogue
+    return do_sweep(c, KPL_SW_INIT_W, 0);
+}
+
+int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t first,
+                       int64_t count, void *workspace, void *stream) {
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
+    if (rc != KPL_OK) return rc;
+    if (op->chunks_global > 0) return fail(KPL_EINVAL, "multi-GPU operators are driven sweep by sweep");
+    for (int64_t j = first; j < first + count; ++j) {
+        if (j % 10 == 0 && (rc = do_sweep(c, KPL_SW_TRUE, j)) != KPL_OK) return rc;
+        if (c.cfg.method == KPL_M_CG) {
+            if ((rc = do_sweep(c, KPL_SW_CG_P, 0)) != KPL_OK) return rc;
+            if ((rc = do_sweep(c, KPL_SW_CG_X, 0)) != KPL_OK) return rc;
+            continue;
+        }
+        if ((rc = do_sweep(c, KPL_SW_ITER, 0)) != KPL_OK) return rc;
+        if (c.cfg.method == KPL_M_PCG_RR) {
+            // explicit replacement, predicated on the device trigger (solvers.py:599-607)
+            for (int k : {KPL_SW_RR_R, KPL_SW_RR_W, KPL_SW_RR_S, KPL_SW_RR_Z})
+                if ((rc = do_sweep(c, k, 0)) != KPL_OK) return rc;
+        }
     }
     return KPL_OK;
 }
 
 int kpl_solver_cg_pass(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t j, int32_t pass,
                        void *workspace, void *stream) {
-    Layout L;
-    int rc = make_layout(op, L);
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
     if (rc != KPL_OK) return rc;
-    if (!cfgp || !v || !workspace) return fail(KPL_EINVAL, "null argument");
-    if (cfgp->method != KPL_M_CG) return fail(KPL_EINVAL, "cg_pass is for classic CG");
-    cudaStream_t st = (cudaStream_t)stream;
-    const Cfg cfg = make_cfg(cfgp);
-    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
-    const bool ident = op->precond == KPL_PC_IDENTITY;
+    if (c.cfg.method != KPL_M_CG) return fail(KPL_EINVAL, "cg_pass is for classic CG");
     if (pass == 1) {
-        if (j % 10 == 0 && (rc = true_residual(op, L, v, ws, cfg, j, PRED_ROW, st)) != KPL_OK) return rc;
-        InCgP in;
-        in.p0 = v->p; in.p1 = v->p1; in.u = ident ? v->r : v->u; in.p = v->p; in.beta = 0.0;
-        BodyCgP bp;
-        bp.p0 = v->p; bp.p1 = v->p1; bp.s = v->s; bp.pout = v->p1;
-        return launch(op, L, in, bp, ws, cfg, PH_CGDELTA, PRED_RUNNING, 0, st);
+        if (j % 10 == 0 && (rc = do_sweep(c, KPL_SW_TRUE, j)) != KPL_OK) return rc;
+        return do_sweep(c, KPL_SW_CG_P, 0);
     }
-    return with_pc(op, [&](auto pc) -> int {
-        constexpr int PC = decltype(pc)::value;
-        BodyCgX<PC> bx;
-        bx.x = v->x; bx.r = v->r; bx.u = v->u; bx.p0 = v->p; bx.p1 = v->p1; bx.s = v->s;
-        bx.dinv = op->inv_diag; bx.c = op->pc_const; bx.alpha = 0.0; bx.p = v->p;
-        return launch(op, L, InNone(), bx, ws, cfg, PH_CGHEAD, PRED_RUNNING, 0, st);
-    });
+    return do_sweep(c, KPL_SW_CG_X, 0);
 }
 
 int kpl_solver_finish(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, void *workspace,
                       void *stream) {
-    Layout L;
-    int rc = make_layout(op, L);
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
     if (rc != KPL_OK) return rc;
-    cudaStream_t st = (cudaStream_t)stream;
-    const Cfg cfg = make_cfg(cfgp);
-    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
     kpl_status s;
     if ((rc = kpl_read_status(workspace, &s, stream)) != KPL_OK) return rc;
     if (s.state != KPL_ST_DONE) return KPL_OK;
     // the final record always carries ||b - A x|| (solvers.py:233-234, `last`);
     // the cadence produced it already iff its slot is no longer NaN
     double have = 0.0;
-    cudaMemcpyAsync(&have, ws.hist + 6 * s.iter + 5, sizeof(double), cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("finish");
+    cudaMemcpyAsync(&have, c.ws.hist + 6 * s.iter + 5, sizeof(double), cudaMemcpyDeviceToHost, c.st);
+    if (cudaStreamSynchronize(c.st) != cudaSuccess) return cuda_check("finish");
     if (!std::isnan(have)) return KPL_OK;
-    return true_residual(op, L, v, ws, cfg, s.iter, PRED_ROW, st);
+    return do_sweep(c, KPL_SW_TRUE, s.iter);
 }
 
-int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfgp, void *workspace, void *stream) {
-    (void)op; (void)cfgp; (void)workspace; (void)stream;
-    return fail(KPL_EUNSUPPORTED, "multi-GPU finalize: not built in this round");
+int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfgp, int32_t kind, int64_t row, void *workspace,
+                        void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if (!cfgp || !workspace) return fail(KPL_EINVAL, "null argument");
+    int phase, pred;
+    if ((rc = kind_phase(kind, phase, pred)) != KPL_OK) return rc;
+    if (phase == PH_NONE) return KPL_OK;
+    const Cfg cfg = make_cfg(cfgp);
+    const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    finalize_kernel<<<1, NT, 0, (cudaStream_t)stream>>>(ws, cfg, phase, pred, row);
+    return cuda_check("finalize");
 }
 
 int kpl_chunk_table(const kpl_op *op, void *workspace, void **local, void **global, int64_t *local_bytes) {

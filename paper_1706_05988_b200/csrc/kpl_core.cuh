@@ -370,18 +370,19 @@ __device__ __forceinline__ bool pred_ok(const WsHead *h, int pred, long long row
 template <int Q>
 __device__ void complete_item(const Ws &ws, const Cfg &cfg, const Layout &L, int phase,
                               long long chunk_local, double *sm) {
+    // Only thread 0 wrote the item partial, so only thread 0 fences (release)
+    // before counting, and fences again (acquire) once it knows it is last.
     __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
     const long long item0 = chunk_local * L.T;
     const long long expect = min((long long)L.T, L.items - item0);   // last CSR chunk may be short
     if (threadIdx.x == 0) {
+        __threadfence();
         const unsigned prev = atomicAdd(&ws.chunk_cnt[chunk_local], 1u);
         s_last = (prev == (unsigned)(expect - 1));
+        if (s_last) __threadfence();
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     double v[Q];
     strided_sum<Q>(ws.items + item0 * NQ, expect, NQ, v, sm);
     const long long cg = ws.chunk_offset + chunk_local;
@@ -391,15 +392,14 @@ __device__ void complete_item(const Ws &ws, const Cfg &cfg, const Layout &L, int
         ws.chunk_cnt[chunk_local] = 0u;
     }
     if (!ws.inline_final) return;
-    __threadfence();
-    __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
         s_last = (prev == (unsigned)(L.nch - 1));
+        if (s_last) __threadfence();
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     double f[Q];
     strided_sum<Q>(ws.chunks, ws.chunks_global, NQ, f, sm);
     if (threadIdx.x == 0) {

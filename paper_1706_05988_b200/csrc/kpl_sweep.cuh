@@ -27,6 +27,7 @@ struct SGeo {
     long long NX, NY, NZ;
     double diag;
     const double *halo_lo, *halo_hi;   // raw stencil-input planes z=-1 / z=NZ (or null)
+    int zhalo;                         // 1: the input vector itself carries planes -1 and NZ
 };
 
 struct CGeo {
@@ -76,9 +77,11 @@ stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int
 
     // raw stencil-input loaders with Dirichlet ghosts / slab halos
     auto plane_ptr = [&](long long zz, long long &off) -> const double * {
-        if (zz < 0) { off = 0; return g.halo_lo; }
-        if (zz >= g.NZ) { off = 0; return g.halo_hi; }
-        off = zz * sxy;
+        if (!g.zhalo) {
+            if (zz < 0) { off = 0; return g.halo_lo; }
+            if (zz >= g.NZ) { off = 0; return g.halo_hi; }
+        }
+        off = zz * sxy;                                // zhalo: planes -1 and NZ are real memory
         return in.base();
     };
     auto ld_own = [&](long long zz, double (&o)[VX]) {
@@ -210,9 +213,10 @@ stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int
 }
 
 template <class In, class Body>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, 3)
 csr_sweep(CGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
     constexpr int Q = Body::NQ;
+    constexpr int PER = CSR_WIN / NT;           // nonzeros staged per thread per window
     __shared__ double sprod[Body::kStencil ? CSR_WIN : 1];
     __shared__ double sred[NQ * NWARP];
     if (!pred_ok(ws.head, pred, row)) return;
@@ -224,38 +228,51 @@ csr_sweep(CGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pre
     const long long r0 = item * RB;
     const long long r = r0 + tid;
     const bool ok = r < g.n;
+    // the body's own-row streams do not depend on the SpMV: issue them first
+    typename Body::template Regs<1> R;
+    if (ok) body.template load<1>(r, R);
     double n[1] = {0.0};
     double cen[1] = {0.0};
     if constexpr (Body::kStencil) {
         const long long rend = min(r0 + RB, g.n);
-        const long long k0 = g.row_ptr[r0], k1 = g.row_ptr[rend];
+        const long long k0 = __ldg(g.row_ptr + r0), k1 = __ldg(g.row_ptr + rend);
         long long lo = 0, hi = 0;
-        if (ok) { lo = g.row_ptr[r]; hi = g.row_ptr[r + 1]; }
+        if (ok) { lo = __ldg(g.row_ptr + r); hi = __ldg(g.row_ptr + r + 1); }
+        if (ok) in.template raw<1>(in.base(), r, cen);
         double a = 0.0;
         for (long long wk = k0; wk < k1; wk += CSR_WIN) {
             const long long we = min(wk + (long long)CSR_WIN, k1);
-            for (long long kk = wk + tid; kk < we; kk += NT) {
-                const int col = __ldcs(g.col_idx + kk);
-                double raw[1];
-                in.template raw<1>(in.base(), col, raw);
-                sprod[kk - wk] = __dmul_rn(__ldcs(g.values + kk), in.xf(raw[0], col));
+            // stage: all index/value loads first, then all gathers (MLP), then products
+            int col[PER];
+            double val[PER], raw[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const long long kk = wk + tid + (long long)j * NT;
+                col[j] = 0; val[j] = 0.0;
+                if (kk < we) { col[j] = __ldcs(g.col_idx + kk); val[j] = __ldcs(g.values + kk); }
+            }
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const long long kk = wk + tid + (long long)j * NT;
+                raw[j] = 0.0;
+                if (kk < we) { double t[1]; in.template raw<1>(in.base(), col[j], t); raw[j] = t[0]; }
+            }
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const long long kk = wk + tid + (long long)j * NT;
+                if (kk < we) sprod[kk - wk] = __dmul_rn(val[j], in.xf(raw[j], col[j]));
             }
             __syncthreads();
             const long long a0 = max(lo, wk), a1 = min(hi, we);
-            for (long long kk = a0; kk < a1; ++kk) a = __dadd_rn(a, sprod[kk - wk]);
+            for (long long kk = a0; kk < a1; ++kk) a = __dadd_rn(a, sprod[kk - wk]);   // csr_matvec order
             __syncthreads();
         }
         n[0] = a;
-        if (ok) in.template raw<1>(in.base(), r, cen);
     }
     double acc[Q > 0 ? Q : 1][1];
 #pragma unroll
     for (int q = 0; q < (Q > 0 ? Q : 1); ++q) acc[q][0] = 0.0;
-    if (ok) {
-        typename Body::template Regs<1> R;
-        body.template load<1>(r, R);
-        body.template compute<1>(r, R, n, cen, acc);
-    }
+    if (ok) body.template compute<1>(r, R, n, cen, acc);
     if constexpr (Q > 0) {
         double t[Q];
 #pragma unroll

@@ -86,7 +86,7 @@ struct TmaRing {
 template <class Body, int D>
 __global__ void __launch_bounds__(NT + 32, 2)
 tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws ws, Cfg cfg, int phase,
-          int pred, long long row, int wsel) {
+          int pred, long long row, int wsel, int wzoff) {
     constexpr int NSTR = Body::kTmaStreams;
     constexpr int SW = TmaRing<D, NSTR>::SW, SS = TmaRing<D, NSTR>::SS;
     constexpr int Q = Body::NQ > 0 ? Body::NQ : 1;
@@ -136,7 +136,7 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
                     const int slot = p % SW;
                     if (p >= SW) mbar_wait(&wempty[slot], ((p / SW) - 1) & 1);
                     mbar_expect_tx(&wfull[slot], TMA_WBYTES);
-                    tma_load3d(wring + slot * TMA_WPLANE, wm, x0 - 2, y0 - 1, z0 - 1 + p, &wfull[slot]);
+                    tma_load3d(wring + slot * TMA_WPLANE, wm, x0 - 2, y0 - 1, z0 - 1 + p + wzoff, &wfull[slot]);
                     ++p;
                 } else {
                     const int slot = q % SS;

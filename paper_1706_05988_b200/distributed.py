@@ -1,0 +1,377 @@
+"""Multi-GPU z-slab solver: one rank per GPU, NCCL for plumbing.
+
+Partition.  A stencil grid (NX, NY, NZ) (2D grids are (nx, 1, ny)) is cut into
+P z-slabs of NZ/P planes.  Each rank stores its slab of every vector plus one
+halo plane below and above (`kpl_op.zhalo = 1`); global-boundary halos stay
+zero (Dirichlet).  Slabs are whole reduction chunks (zc | NZ/P), so each
+rank's chunk partials are exactly the partials a single GPU would compute for
+those planes.
+
+Per sweep.  halo exchange of the sweep's stencil input (plane 0 -> rank-1's
+upper halo, plane nz-1 -> rank+1's lower halo; NCCL send/recv over NVLink) ->
+the fused sweep on the local slab (writes this rank's slice of the chunk
+table) -> all-gather of the chunk table (P x chunks x 32 bytes) -> the
+level-4 fold + scalar epilogue on every rank (identical inputs, identical
+scalars).  Because the chunk partials and the fold order do not depend on P,
+a P-rank solve is bit-identical to the 1-GPU solve.
+
+Communicators.  `TorchComm` wraps torch.distributed (NCCL on GPUs, gloo on
+CPU for the plumbing tests).  `LocalComm` runs P ranks as P slab states in
+one process on one device (exchanges and gathers become device copies; all
+sweeps are launched sequentially, none waits on another) -- the single-GPU
+stand-in used by the parity tests.
+
+Scope: stencil operators, identity or constant-diagonal Jacobi, methods
+cg / pcg / pcg_sh / pcg_rr.  Row-block CSR with general halo gathers is not
+built yet (raises NotImplementedError).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _lib, device as D
+from .solvers import (BreakdownError, IterationRecord, SolveResult, SolverConfig, _CODE)
+
+_ZC_CHOICES = (16, 8, 4, 2, 1)
+
+
+class SlabPlan:
+    """z-slab partition of an (NX, NY, NZ) grid over P ranks."""
+
+    def __init__(self, NX, NY, NZ, P, zc=0):
+        if NZ % P:
+            raise ValueError(f"NZ={NZ} planes do not split evenly over {P} ranks")
+        self.NX, self.NY, self.NZ, self.P = NX, NY, NZ, P
+        self.nzl = NZ // P
+        if zc <= 0:
+            zc = next(c for c in _ZC_CHOICES if self.nzl % c == 0)
+        if self.nzl % zc:
+            raise ValueError(f"chunk length zc={zc} must divide the slab depth {self.nzl}")
+        self.zc = zc
+        self.sxy = NX * NY
+        self.n_local = self.sxy * self.nzl
+        self.chunks_local = self.nzl // zc
+        self.chunks_global = self.chunks_local * P
+
+    def z0(self, rank):
+        return rank * self.nzl
+
+    def local_slice(self, rank):
+        """Slice of a global natural-order vector owned by `rank`."""
+        a = rank * self.n_local
+        return slice(a, a + self.n_local)
+
+
+class _RankState:
+    """Device state of one rank (vectors with halo planes, op, workspace)."""
+
+    VEC_NAMES = ("x", "r", "u", "w0", "w1", "z", "q", "s", "t", "p", "p1")
+
+    def __init__(self, plan: SlabPlan, rank, diag, pc_code, pc_const, cfg: SolverConfig, device):
+        t = D.torch()
+        self.plan, self.rank, self.device = plan, rank, device
+        self.cfg = cfg
+        self.ident = pc_code == _lib.KPL_PC_IDENTITY
+        n, sxy = plan.n_local, plan.sxy
+        f64 = dict(dtype=t.float64, device=device)
+        self.full = {}                  # name -> (nzl+2)*sxy tensor incl. halos
+
+        def vec():
+            return t.zeros(n + 2 * sxy, **f64)
+
+        names = ["x", "r"]
+        if not self.ident:
+            names.append("u")
+        if cfg.method == "cg":
+            names += ["p", "p1", "s"]
+        else:
+            names += ["w0", "w1", "z", "s", "t"]
+            if not self.ident:
+                names += ["q", "p"]
+        for nm in names:
+            self.full[nm] = vec()
+        if self.ident:
+            self.full["u"] = self.full["r"]
+            if cfg.method != "cg":
+                self.full["q"] = self.full["s"]
+                self.full["p"] = self.full["t"]
+        self.b = t.zeros(n, **f64)
+
+        op = _lib.KplOp()
+        op.kind = _lib.KPL_OP_STENCIL
+        op.precond = pc_code
+        op.n = n
+        op.nx, op.ny, op.nz, op.diag = plan.NX, plan.NY, plan.nzl, float(diag)
+        op.zc = plan.zc
+        op.zhalo = 1
+        op.pc_const = pc_const
+        op.chunk_offset = rank * plan.chunks_local
+        op.chunks_global = plan.chunks_global
+        self.op = op
+
+        c = _lib.KplCfg()
+        c.method = _CODE[cfg.method]
+        c.shift = float(cfg.shift)
+        c.max_iters = int(cfg.max_iters)
+        c.rtol = float(cfg.rtol)
+        c.rr_threshold = float(cfg.rr_threshold)
+        self.kcfg = c
+
+        v = _lib.KplVecs()
+        for nm in self.VEC_NAMES:
+            setattr(v, nm, D.ptr(self.interior(nm)) if nm in self.full else None)
+        v.b = D.ptr(self.b)
+        self.vecs = v
+
+        lib = _lib.load()
+        nbytes = lib.kpl_workspace_bytes(op, cfg.max_iters)
+        _lib.check(nbytes if nbytes < 0 else 0, "workspace size")
+        self.ws = t.empty(int(nbytes), dtype=t.uint8, device=device)
+        loc, glob, lbytes = _lib._p(), _lib._p(), _lib._i64()
+        _lib.check(lib.kpl_chunk_table(op, D.ptr(self.ws), loc, glob, lbytes), "chunk table")
+        base = self.ws.data_ptr()
+        g0 = glob.value - base
+        l0 = loc.value - base
+        nb = 8 * 4 * plan.chunks_global
+        self.table = self.ws[g0:g0 + nb].view(t.float64)
+        self.table_local = self.ws[l0:l0 + lbytes.value].view(t.float64)
+        self.hist_off = lib.kpl_history_offset(op)
+        self.reps_off = lib.kpl_replacements_offset(op, cfg.max_iters)
+        self.status = _lib.KplStatus()
+
+    def interior(self, name):
+        sxy = self.plan.sxy
+        return self.full[name][sxy:sxy + self.plan.n_local]
+
+    def planes(self, name):
+        """(lower halo, first plane, last plane, upper halo) views."""
+        f, sxy, n = self.full[name], self.plan.sxy, self.plan.n_local
+        return f[:sxy], f[sxy:2 * sxy], f[n:n + sxy], f[n + sxy:]
+
+    # -- device calls
+    def prepare(self):
+        _lib.check(_lib.load().kpl_solver_prepare(self.op, self.kcfg, self.vecs, D.ptr(self.ws),
+                                                  D.stream_handle()), "prepare")
+
+    def sweep(self, kind, row=0):
+        _lib.check(_lib.load().kpl_sweep(self.op, self.kcfg, self.vecs, kind, row, D.ptr(self.ws),
+                                         D.stream_handle()), f"sweep {kind}")
+
+    def finalize(self, kind, row=0):
+        _lib.check(_lib.load().kpl_finalize_global(self.op, self.kcfg, kind, row, D.ptr(self.ws),
+                                                   D.stream_handle()), f"finalize {kind}")
+
+    def read_status(self):
+        _lib.check(_lib.load().kpl_read_status(D.ptr(self.ws), self.status, D.stream_handle()),
+                   "status")
+        return self.status
+
+    def history(self, rows):
+        t = D.torch()
+        raw = self.ws[self.hist_off:self.hist_off + 48 * rows]
+        return raw.view(t.float64).reshape(rows, 6).cpu().numpy()
+
+
+class LocalComm:
+    """P ranks as P slab states in one process on one device."""
+
+    def __init__(self, P):
+        self.size = P
+        self.rank = None                 # all ranks are local
+
+    def local_ranks(self):
+        return list(range(self.size))
+
+    def exchange(self, states, name):
+        for s in states:
+            r = s.rank
+            lo, first, last, hi = s.planes(name)
+            if r > 0:
+                lo.copy_(states[r - 1].planes(name)[2])
+            if r < self.size - 1:
+                hi.copy_(states[r + 1].planes(name)[1])
+
+    def allgather(self, states):
+        for dst in states:
+            for src in states:
+                if src is not dst:
+                    n = src.table_local.numel()
+                    off = src.rank * n
+                    dst.table[off:off + n].copy_(src.table_local)
+
+
+class TorchComm:
+    """torch.distributed process group (NCCL over NVLink on GPUs; gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.size = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def local_ranks(self):
+        return [self.rank]
+
+    def exchange(self, states, name):
+        dist = self.dist
+        (s,) = states
+        lo, first, last, hi = s.planes(name)
+        ops = []
+        if s.rank > 0:
+            ops.append(dist.P2POp(dist.isend, first.contiguous(), s.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, lo, s.rank - 1, self.group))
+        if s.rank < self.size - 1:
+            ops.append(dist.P2POp(dist.isend, last.contiguous(), s.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, hi, s.rank + 1, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def allgather(self, states):
+        (s,) = states
+        # in-place all-gather: this rank's slice already sits at offset rank*count
+        self.dist.all_gather_into_tensor(s.table, s.table_local.clone(), group=self.group)
+
+
+class DistributedStencilSolve:
+    """Drive one z-slab-partitioned solve; `comm` decides which ranks are local."""
+
+    def __init__(self, A, M, cfg: SolverConfig, comm, zc=0):
+        if not hasattr(A, "stencil_spec"):
+            raise NotImplementedError("multi-GPU row-block CSR (general halo gather) is not built yet")
+        if cfg.track_gaps or cfg.method == "pcg_var_sh":
+            raise NotImplementedError("track_gaps / pcg_var_sh are not on the device path yet")
+        self.device = D.require_cuda()
+        NX, NY, NZ, diag = A.stencil_spec()
+        self.A, self.cfg, self.comm = A, cfg, comm
+        self.plan = SlabPlan(NX, NY, NZ, comm.size, zc)
+        kind = "identity" if M is None else getattr(M, "kind", "identity")
+        if kind == "identity":
+            pc, c = _lib.KPL_PC_IDENTITY, 0.0
+        elif kind == "jacobi":
+            c = getattr(M, "inv_const", None)
+            if c is None:
+                inv = np.asarray(M.inv_diag)
+                if not np.all(inv == inv[0]):
+                    raise ValueError("stencil operators need a constant Jacobi diagonal")
+                c = float(inv[0])
+            pc = _lib.KPL_PC_JACOBI_CONST
+        else:
+            raise NotImplementedError(f"preconditioner {kind!r} not on the device path")
+        self.states = [_RankState(self.plan, r, diag, pc, c, cfg, self.device)
+                       for r in comm.local_ranks()]
+        if cfg.method == "pcg_rr":
+            coef = (A.mu * math.sqrt(A.n) + 1.0) * A.norm_inf()
+            for s in self.states:
+                s.kcfg.rr_coef = coef
+        self.limit = cfg.max_iters + (1 if cfg.method == "cg" else 0)
+
+    # -- collective building blocks
+    def _all(self, fn):
+        for s in self.states:
+            fn(s)
+
+    def exchange(self, name):
+        self.comm.exchange(self.states, name)
+
+    def sweep(self, kind, row=0, inputs=()):
+        for nm in inputs:
+            self.exchange(nm)
+        self._all(lambda s: s.sweep(kind, row))
+        if _lib.load().kpl_sweep_phase(kind) != 0:
+            self.comm.allgather(self.states)
+            self._all(lambda s: s.finalize(kind, row))
+
+    # -- public
+    def load_rhs(self, b_local_list, x0_local_list=None):
+        """Per local rank: its slab of b (and x0), any array-like of length n_local."""
+        t = D.torch()
+        for i, s in enumerate(self.states):
+            s.b.copy_(t.as_tensor(np.asarray(b_local_list[i]) if not isinstance(b_local_list[i], t.Tensor)
+                                  else b_local_list[i], dtype=t.float64))
+            x = s.interior("x")
+            if x0_local_list is None:
+                x.zero_()
+            else:
+                v = x0_local_list[i]
+                x.copy_(v if isinstance(v, t.Tensor) else t.as_tensor(np.asarray(v), dtype=t.float64))
+
+    def init(self):
+        m = self.cfg.method
+        self._all(lambda s: s.prepare())
+        self.sweep(_lib.KPL_SW_BNORM)
+        self.sweep(_lib.KPL_SW_INIT_R, inputs=("x",))
+        if m != "cg":
+            self.sweep(_lib.KPL_SW_INIT_W, inputs=("u",))
+        self.issued = 0
+
+    def step(self):
+        """One iteration (host index j = self.issued)."""
+        j = self.issued
+        m = self.cfg.method
+        if j % 10 == 0:
+            self.sweep(_lib.KPL_SW_TRUE, row=j, inputs=("x",))
+        if m == "cg":
+            par = "p1" if (j & 1) else "p"
+            self.sweep(_lib.KPL_SW_CG_P, inputs=(par, "u"))
+            self.sweep(_lib.KPL_SW_CG_X)
+        else:
+            self.sweep(_lib.KPL_SW_ITER, inputs=("w1" if (j & 1) else "w0",))
+            if m == "pcg_rr":
+                self.sweep(_lib.KPL_SW_RR_R, inputs=("x",))
+                self.sweep(_lib.KPL_SW_RR_W, inputs=("u",))
+                self.sweep(_lib.KPL_SW_RR_S, inputs=("p",))
+                self.sweep(_lib.KPL_SW_RR_Z, inputs=("q",))
+        self.issued += 1
+
+    def run(self, poll=16):
+        self.init()
+        st = self.states[0].read_status()
+        while st.state == _lib.KPL_ST_RUNNING and self.issued < self.limit:
+            for _ in range(min(poll, self.limit - self.issued)):
+                self.step()
+            st = self.states[0].read_status()
+        return self.result()
+
+    def result(self):
+        s0 = self.states[0]
+        st = s0.read_status()
+        if st.state == _lib.KPL_ST_BREAKDOWN:
+            msg = _lib.load().kpl_breakdown_message(st.bd_code).decode()
+            raise BreakdownError(int(st.bd_iter), msg)
+        if st.state != _lib.KPL_ST_DONE:
+            raise _lib.KplError(f"distributed solve ended in state {st.state}")
+        rows = int(st.iter) + 1
+        if np.isnan(s0.history(rows)[-1, 5]):
+            self.sweep(_lib.KPL_SW_TRUE, row=int(st.iter), inputs=("x",))
+        h = s0.history(rows)
+        history = [IterationRecord(i, *(float(c) for c in h[i, :5]),
+                                   rnorm_true=None if np.isnan(h[i, 5]) else float(h[i, 5]))
+                   for i in range(rows)]
+        reps = []
+        if st.n_replacements:
+            t = D.torch()
+            raw = s0.ws[s0.reps_off:s0.reps_off + 8 * int(st.n_replacements)]
+            reps = [int(v) for v in raw.view(t.int64).cpu().numpy()]
+        xs = [s.interior("x").clone() for s in self.states]
+        return SolveResult(xs, bool(st.converged), rows - 1, history, reps)
+
+
+def solve_distributed(A, M, b_local, x0_local, cfg: SolverConfig, comm=None, zc=0):
+    """z-slab solve on the ranks of `comm` (default: the torch.distributed world).
+
+    `b_local` / `x0_local`: this rank's slab (natural order, n/P values), or,
+    with a LocalComm, a list with one slab per rank.  Returns a SolveResult
+    whose `x` is the list of local slabs and whose history is global."""
+    if comm is None:
+        comm = TorchComm()
+    S = DistributedStencilSolve(A, M, cfg, comm, zc=zc)
+    if not isinstance(comm, LocalComm):
+        b_local = [b_local]
+        x0_local = None if x0_local is None else [x0_local]
+    S.load_rhs(b_local, x0_local)
+    return S.run()

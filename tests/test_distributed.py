@@ -1,0 +1,177 @@
+"""Multi-GPU z-slab path.
+
+CPU (gloo, world_size 2): partition plan, the halo exchange + chunk-table
+all-gather plumbing of TorchComm, and the partition invariance of the
+reduction order (per-rank chunk partials + gathered level-4 fold == the
+single-GPU tree).
+
+GPU (one device, P virtual ranks via LocalComm): a P-rank solve is bit-identical
+to the 1-GPU solve, for every method, 2D and 3D, identity and Jacobi.
+"""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gpu_order
+from paper_1706_05988_b200.distributed import SlabPlan, TorchComm
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_slab_plan():
+    p = SlabPlan(512, 512, 512, 8)
+    assert p.nzl == 64 and p.zc == 16 and p.chunks_local == 4 and p.chunks_global == 32
+    assert p.local_slice(3) == slice(3 * 512 * 512 * 64, 4 * 512 * 512 * 64)
+    with pytest.raises(ValueError):
+        SlabPlan(8, 8, 10, 4)
+    with pytest.raises(ValueError):
+        SlabPlan(8, 8, 16, 2, zc=16)
+    assert SlabPlan(8, 8, 24, 2).zc == 4
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("dims,vx,wx,wy", [((64, 10, 32), 2, 1, 8), ((200, 1, 64), 2, 8, 1)])
+def test_reduction_partition_invariant(P, dims, vx, wx, wy):
+    """Level 1-3 per slab, gather, level 4 == the single-GPU tree (bitwise)."""
+    NX, NY, NZ = dims
+    rng = np.random.default_rng(0)
+    u, v = rng.normal(size=NX * NY * NZ), rng.normal(size=NX * NY * NZ)
+    zc = 4
+    whole = gpu_order.stencil_dot_fn(NX, NY, NZ, vx, wx, wy, zc)(u, v)
+    plan = SlabPlan(NX, NY, NZ, P, zc)
+    chunks = []
+    for r in range(P):
+        sl = plan.local_slice(r)
+        items = gpu_order.stencil_item_partials(u[sl] * v[sl], NX, NY, plan.nzl, vx, wx, wy, zc)
+        chunks += list(items)
+    assert gpu_order.reduce_items(chunks) == whole
+
+
+class _FakeState:
+    """Stand-in rank state with CPU tensors (plumbing test only)."""
+
+    def __init__(self, rank, P, sxy, nzl, chunks):
+        self.rank = rank
+        self.sxy, self.nzl = sxy, nzl
+        self.full = {"w0": torch.zeros((nzl + 2) * sxy, dtype=torch.float64)}
+        self.full["w0"][sxy:(nzl + 1) * sxy] = torch.arange(nzl * sxy, dtype=torch.float64) + 1000 * rank
+        self.table = torch.zeros(P * chunks * 4, dtype=torch.float64)
+        self.table_local = self.table[rank * chunks * 4:(rank + 1) * chunks * 4]
+        self.table_local.copy_(torch.arange(chunks * 4, dtype=torch.float64) + 100 * rank)
+
+    def planes(self, name):
+        f, sxy, n = self.full[name], self.sxy, self.sxy * self.nzl
+        return f[:sxy], f[sxy:2 * sxy], f[n:n + sxy], f[n + sxy:]
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        sxy, nzl, chunks = 6, 3, 2
+        s = _FakeState(rank, world, sxy, nzl, chunks)
+        comm.exchange([s], "w0")
+        comm.allgather([s])
+        lo, first, last, hi = s.planes("w0")
+        q.put((rank, lo.tolist(), hi.tolist(), s.table.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_halo_exchange_and_table_allgather():
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, lo, hi, table = q.get(timeout=120)
+        out[r] = (lo, hi, table)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sxy, nzl = 6, 3
+    # rank 0: lower halo is the Dirichlet zero plane, upper halo = rank 1's first plane
+    assert out[0][0] == [0.0] * sxy
+    assert out[0][1] == [1000.0 + k for k in range(sxy)]
+    # rank 1: lower halo = rank 0's last plane, upper halo zero
+    assert out[1][0] == [float((nzl - 1) * sxy + k) for k in range(sxy)]
+    assert out[1][1] == [0.0] * sxy
+    want = [float(k) for k in range(8)] + [100.0 + k for k in range(8)]
+    assert out[0][2] == want and out[1][2] == want
+
+
+# ----------------------------------------------------------------- GPU
+
+gpu = pytest.mark.gpu
+
+
+def _one_gpu(A, M, b, cfg, zc):
+    from paper_1706_05988_b200.solvers import _Solve
+    return _Solve(A, M, b, None, cfg, zc=zc).run()
+
+
+@gpu
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("method,extra", [("pcg_sh", {"shift": 2.30188679245283}), ("pcg", {}),
+                                          ("cg", {}), ("pcg_rr", {})])
+def test_local_ranks_bitwise_3d(P, method, extra):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200.distributed import LocalComm, SlabPlan, solve_distributed
+    A = K.Stencil3D(64, 24, 32)
+    b = K.spmv(A, np.random.default_rng(2).normal(size=A.n))
+    cfg = K.SolverConfig(method=method, max_iters=80, rtol=1e-10, **extra)
+    zc = 4
+    ref = _one_gpu(A, None, b, cfg, zc)
+    plan = SlabPlan(64, 24, 32, P, zc)
+    res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
+                            comm=LocalComm(P), zc=zc)
+    x = np.concatenate([xi.cpu().numpy() for xi in res.x])
+    assert res.iterations == ref.iterations
+    for a, c in zip(res.history, ref.history):
+        assert (a.alpha, a.beta, a.gamma, a.delta, a.rnorm_recursive, a.rnorm_true) == \
+               (c.alpha, c.beta, c.gamma, c.delta, c.rnorm_recursive, c.rnorm_true)
+    assert x.tobytes() == ref.x.tobytes()
+    assert res.replacements == ref.replacements
+
+
+@gpu
+@pytest.mark.parametrize("P", [2, 3])
+def test_local_ranks_bitwise_2d_jacobi(P):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200.distributed import LocalComm, SlabPlan, solve_distributed
+    A = K.Stencil2D(96, 48)
+    M = K.make_jacobi(A)
+    b = K.spmv(A, np.random.default_rng(0).random(A.n))
+    cfg = K.SolverConfig(method="pcg_sh", shift=0.49238826317067413, max_iters=300, rtol=1e-10)
+    zc = 2
+    ref = _one_gpu(A, M, b, cfg, zc)
+    plan = SlabPlan(96, 1, 48, P, zc)
+    res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
+                            comm=LocalComm(P), zc=zc)
+    x = np.concatenate([xi.cpu().numpy() for xi in res.x])
+    assert res.iterations == ref.iterations and res.converged
+    assert [r.alpha for r in res.history] == [r.alpha for r in ref.history]
+    assert x.tobytes() == ref.x.tobytes()
