@@ -198,7 +198,7 @@ def run_ours(args):
     barrier()
     t_e2e = max_over_ranks(f0.elapsed_time(f1) / 1000.0)
     e2e = world * r2.iterations * args.steps / t_e2e
-    hist_bytes = 48 * (r2.iterations + 1)
+    hist_bytes = 80 * (r2.iterations + 1)
 
     # ---- dominant kernel: the fused p-CG-sh iteration sweep, timed alone
     S = _Solve(A, None, b, None, K.SolverConfig(method="pcg_sh", shift=SIGMA, max_iters=100, rtol=0.0))

@@ -77,19 +77,21 @@ typedef struct kpl_op {
 } kpl_op;
 
 /* ---- solver configuration (mirror of SolverConfig, solvers.py:60-86) ---- */
-#define KPL_M_CG      0
-#define KPL_M_PCG     1
-#define KPL_M_PCG_SH  2
-#define KPL_M_PCG_RR  4
+#define KPL_M_CG         0
+#define KPL_M_PCG        1
+#define KPL_M_PCG_SH     2
+#define KPL_M_PCG_VAR_SH 3
+#define KPL_M_PCG_RR     4
 
 typedef struct kpl_cfg {
     int32_t method;          /* KPL_M_*                                          */
-    int32_t _pad0;
+    int32_t track_gaps;      /* 1: gap norms + true residual at every record      */
     double  shift;           /* sigma (pcg_sh)                                    */
     int64_t max_iters;
     double  rtol;
     double  rr_threshold;    /* tau (pcg_rr)                                      */
     double  rr_coef;         /* (mu*sqrt(n)+1)*norm_inf(A)  (solvers.py:514)      */
+    const double *shift_schedule;  /* DEVICE, max_iters+1 values (pcg_var_sh)     */
 } kpl_cfg;
 
 /* Solver vectors (device, length n).  With KPL_PC_IDENTITY the reference's
@@ -118,9 +120,10 @@ typedef struct kpl_status {
     int64_t _pad[9];
 } kpl_status;
 
-/* History row layout (fp64, 6 columns, row i = record i):
-   alpha, beta, gamma, delta, rnorm_recursive, rnorm_true (NaN = None).     */
-#define KPL_HIST_COLS 6
+/* History row layout (fp64, 10 columns, row i = record i; NaN = None):
+   alpha, beta, gamma, delta, rnorm_recursive, rnorm_true, gap_f, gap_g,
+   gap_h, gap_j  (IterationRecord, solvers.py:89-101).                       */
+#define KPL_HIST_COLS 10
 
 /* ---- sizing / introspection -------------------------------------------- */
 int64_t kpl_workspace_bytes(const kpl_op *op, int64_t max_iters);
@@ -188,6 +191,10 @@ int kpl_read_status(const void *workspace, kpl_status *out, void *stream);
 #define KPL_SW_RR_W    9   /* replacement w = A u (:602)                          */
 #define KPL_SW_RR_S   10   /* replacement s = A p, q = M s (:603-604)             */
 #define KPL_SW_RR_Z   11   /* replacement z = A q + next reductions (:605)        */
+#define KPL_SW_GAP_F  12   /* track_gaps: ||b-Ax||, ||f|| at row `row` (:148-149) */
+#define KPL_SW_GAP_G  13   /* ||axpy(-sigma, t, A p) - s|| (:153)                 */
+#define KPL_SW_GAP_H  14   /* ||axpy(-sigma, r, A u) - w|| (:152)                 */
+#define KPL_SW_GAP_J  15   /* ||A q - z|| (:154)                                  */
 /* Reset the workspace head/history and zero the state vectors that start at 0. */
 int kpl_solver_prepare(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, void *workspace,
                        void *stream);

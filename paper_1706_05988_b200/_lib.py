@@ -19,11 +19,12 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "kpl_b200.h")
 KPL_OK, KPL_EINVAL, KPL_ECUDA, KPL_EUNSUPPORTED = 0, -1, -2, -3
 KPL_OP_STENCIL, KPL_OP_CSR = 1, 2
 KPL_PC_IDENTITY, KPL_PC_JACOBI_CONST, KPL_PC_JACOBI_VEC = 0, 1, 2
-KPL_M_CG, KPL_M_PCG, KPL_M_PCG_SH, KPL_M_PCG_RR = 0, 1, 2, 4
+KPL_M_CG, KPL_M_PCG, KPL_M_PCG_SH, KPL_M_PCG_VAR_SH, KPL_M_PCG_RR = 0, 1, 2, 3, 4
 KPL_ST_RUNNING, KPL_ST_DONE, KPL_ST_BREAKDOWN = 0, 1, 2
-KPL_HIST_COLS = 6
+KPL_HIST_COLS = 10
 (KPL_SW_BNORM, KPL_SW_INIT_R, KPL_SW_INIT_W, KPL_SW_ITER, KPL_SW_TRUE, KPL_SW_CG_P, KPL_SW_CG_X,
- KPL_SW_RR_R, KPL_SW_RR_W, KPL_SW_RR_S, KPL_SW_RR_Z) = range(1, 12)
+ KPL_SW_RR_R, KPL_SW_RR_W, KPL_SW_RR_S, KPL_SW_RR_Z,
+ KPL_SW_GAP_F, KPL_SW_GAP_G, KPL_SW_GAP_H, KPL_SW_GAP_J) = range(1, 16)
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -41,8 +42,8 @@ class KplOp(ctypes.Structure):
 
 
 class KplCfg(ctypes.Structure):
-    _fields_ = [("method", _i32), ("_pad0", _i32), ("shift", _d), ("max_iters", _i64),
-                ("rtol", _d), ("rr_threshold", _d), ("rr_coef", _d)]
+    _fields_ = [("method", _i32), ("track_gaps", _i32), ("shift", _d), ("max_iters", _i64),
+                ("rtol", _d), ("rr_threshold", _d), ("rr_coef", _d), ("shift_schedule", _p)]
 
 
 class KplVecs(ctypes.Structure):

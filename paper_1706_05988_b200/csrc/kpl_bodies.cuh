@@ -222,7 +222,12 @@ struct BodyInitW {
 // PC == IDENTITY: u, q, p alias r, s, t (bitwise equal in the reference) and
 // are neither loaded nor stored.  Partials: gamma=(r,u), delta=(sigma r + w, u),
 // rho=(r,r), xi=(x,x) (pcg_rr trigger only).
-template <int PC>
+//
+// VAR (pcg_var_sh, solvers.py:479-495): the shift changes from sigma_prev =
+// schedule[i] to sigma_cur = schedule[i+1]; dsig = sigma_cur - sigma_prev
+// enters the s, q, z and w recurrences with the reference's evaluation order
+// (t, p first; s, q; z; x; w before r, which it reads).
+template <int PC, bool VAR = false>
 struct BodyPcgIter {
     static constexpr int NQ = 4;
     static constexpr bool kStencil = true;
@@ -233,6 +238,8 @@ struct BodyPcgIter {
     int want_xi;
     double alpha, beta, asig;
     double *wout;
+    const double *schedule;
+    double dsig;
     template <int V> struct Regs { double x[V], r[V], z[V], s[V], t[V], u[V], q[V], p[V], d[V]; };
     static constexpr int kTmaStreams = 5;                 // x, r, z, s, t (identity preconditioner)
     __device__ void load_tma(const double *S, int cs, Regs<2> &R) const {
@@ -241,7 +248,13 @@ struct BodyPcgIter {
     __device__ void setup(const Ws &ws) {
         alpha = ws.head->alpha;
         beta = ws.head->beta;
-        asig = __dmul_rn(alpha, sigma);                 // solvers.py:416
+        if constexpr (VAR) {
+            const long long i = ws.head->iter;
+            const double sp = schedule[i];
+            sigma = schedule[i + 1];                    // sigma_cur; also the next delta's shift
+            dsig = __dsub_rn(sigma, sp);                // solvers.py:481
+        }
+        asig = __dmul_rn(alpha, sigma);                 // solvers.py:416 / :493
         wout = const_cast<double *>(pick(ws.head, SEL_ITER1, w0, w1));
     }
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
@@ -269,21 +282,32 @@ struct BodyPcgIter {
             else if constexpr (PC == KPL_PC_JACOBI_CONST) m = __dmul_rn(w, c);
             else m = __dmul_rn(w, R.d[v]);
             const double uin = (PC == KPL_PC_IDENTITY) ? R.r[v] : R.u[v];
-            zo[v] = axpy1(beta, R.z[v], n[v]);                  // z = axpy(beta, z, n)
-            so[v] = axpy1(beta, R.s[v], w);                     // s = axpy(beta, s, w)
-            to[v] = axpy1(beta, R.t[v], R.r[v]);                // t = axpy(beta, t, r)
             double qn, pn;
-            if constexpr (PC == KPL_PC_IDENTITY) { qn = so[v]; pn = to[v]; }
-            else {
-                qn = axpy1(beta, R.q[v], m);                    // q = axpy(beta, q, m)
-                pn = axpy1(beta, R.p[v], uin);                  // p = axpy(beta, p, u)
+            if constexpr (!VAR) {
+                zo[v] = axpy1(beta, R.z[v], n[v]);              // z = axpy(beta, z, n)
+                so[v] = axpy1(beta, R.s[v], w);                 // s = axpy(beta, s, w)
+                to[v] = axpy1(beta, R.t[v], R.r[v]);            // t = axpy(beta, t, r)
+                if constexpr (PC == KPL_PC_IDENTITY) { qn = so[v]; pn = to[v]; }
+                else {
+                    qn = axpy1(beta, R.q[v], m);                // q = axpy(beta, q, m)
+                    pn = axpy1(beta, R.p[v], uin);              // p = axpy(beta, p, u)
+                }
+            } else {
+                const double md = -dsig;
+                to[v] = axpy1(beta, R.t[v], R.r[v]);            // t = axpy(beta, t, r)
+                pn = (PC == KPL_PC_IDENTITY) ? to[v] : axpy1(beta, R.p[v], uin);   // p = axpy(beta, p, u)
+                so[v] = axpy1(md, to[v], axpy1(beta, R.s[v], w));                  // s = axpy(-dsig, t, axpy(beta, s, w))
+                qn = (PC == KPL_PC_IDENTITY) ? so[v] : axpy1(md, pn, axpy1(beta, R.q[v], m));
+                const double zb = axpy1(beta, R.z[v], n[v]);    // zbase = axpy(beta, z, n)
+                zo[v] = dsig == 0.0 ? zb : axpy1(md, axpy1(sigma, to[v], so[v]), zb);
             }
             qo[v] = qn; po[v] = pn;
             xo[v] = axpy1(alpha, pn, R.x[v]);                   // x = axpy(alpha, p, x)
+            if constexpr (VAR) wo[v] = sub2(w, alpha, zo[v], dsig, R.r[v]);   // w = _sub2(w, a, z, dsig, r)
             ro[v] = sub2(R.r[v], alpha, so[v], asig, to[v]);    // r = _sub2(r, a, s, asig, t)
             if constexpr (PC == KPL_PC_IDENTITY) uo[v] = ro[v];
             else uo[v] = sub2(uin, alpha, qn, asig, pn);        // u = _sub2(u, a, q, asig, p)
-            wo[v] = __dsub_rn(w, __dmul_rn(alpha, zo[v]));      // w = w - alpha*z
+            if constexpr (!VAR) wo[v] = __dsub_rn(w, __dmul_rn(alpha, zo[v]));   // w = w - alpha*z
             const double dv = axpy1(sigma, ro[v], wo[v]);       // axpy(sigma, r, w)
             acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(ro[v], uo[v]));
             acc[1][v] = __dadd_rn(acc[1][v], __dmul_rn(dv, uo[v]));
@@ -300,6 +324,53 @@ struct BodyPcgIter {
             st_cs<V>(u, k, uo);
             st_cs<V>(q, k, qo);
             st_cs<V>(p, k, po);
+        }
+    }
+};
+
+// track_gaps record sweeps (solvers.py:142-167, gap_vectors / measure_gaps):
+//   F: input x;  t = b - A x -> (t,t), (t - r, t - r)
+//   G: input p;  axpy(-sigma_prev, t, A p) - s
+//   H: input u;  axpy(-sigma_prev, r, A u) - w
+//   J: input q;  A q - z
+// sigma_prev is the record's shift (schedule[i] for pcg_var_sh).
+enum GapMode : int { GAP_F = 0, GAP_G = 1, GAP_H = 2, GAP_J = 3 };
+
+template <int MODE>
+struct BodyGap {
+    static constexpr int NQ = MODE == GAP_F ? 2 : 1;
+    static constexpr bool kStencil = true;
+    const double *b, *r, *t, *s, *z, *w0, *w1;
+    const double *schedule;
+    double sig;
+    const double *w;
+    template <int V> struct Regs { double a[V], c[V]; };
+    __device__ void setup(const Ws &ws) {
+        w = pick(ws.head, SEL_ITER, w0, w1);
+        if (schedule) sig = schedule[ws.head->iter];
+    }
+    template <int V> __device__ void load(long long k, Regs<V> &R) const {
+        if constexpr (MODE == GAP_F) { ld_cs<V>(b, k, R.a); ld_cs<V>(r, k, R.c); }
+        if constexpr (MODE == GAP_G) { ld_cs<V>(t, k, R.a); ld_cs<V>(s, k, R.c); }
+        if constexpr (MODE == GAP_H) { ld_cs<V>(r, k, R.a); ld_cs<V>(w, k, R.c); }
+        if constexpr (MODE == GAP_J) { ld_cs<V>(z, k, R.c); }
+    }
+    template <int V>
+    __device__ void compute(long long, const Regs<V> &R, const double (&n)[V], const double (&)[V],
+                            double (&acc)[NQ][V]) const {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if constexpr (MODE == GAP_F) {
+                const double tr = __dsub_rn(R.a[v], n[v]);
+                const double f = __dsub_rn(tr, R.c[v]);
+                acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(tr, tr));
+                acc[1][v] = __dadd_rn(acc[1][v], __dmul_rn(f, f));
+            } else {
+                double g;
+                if constexpr (MODE == GAP_J) g = __dsub_rn(n[v], R.c[v]);
+                else g = __dsub_rn(axpy1(-sig, R.a[v], n[v]), R.c[v]);
+                acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(g, g));
+            }
         }
     }
 };

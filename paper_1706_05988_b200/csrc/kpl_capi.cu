@@ -92,7 +92,7 @@ Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     o.chunks = o.items + align256(8LL * NQ * L.items);
     o.cnt = o.chunks + align256(8LL * NQ * cg);
     o.hist = o.cnt + align256(4LL * L.nch);
-    o.reps = o.hist + align256(48LL * (max_iters + 1));
+    o.reps = o.hist + align256(8LL * HC * (max_iters + 1));
     o.total = o.reps + align256(8LL * (max_iters + 1));
     return o;
 }
@@ -116,6 +116,8 @@ Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspa
 Cfg make_cfg(const kpl_cfg *c) {
     Cfg k;
     k.method = c ? c->method : KPL_M_PCG_SH;
+    k.track_gaps = c ? c->track_gaps : 0;
+    k.schedule = c ? c->shift_schedule : nullptr;
     k.shift = c ? c->shift : 0.0;
     k.rtol = c ? c->rtol : 0.0;
     k.tau = c ? c->rr_threshold : 0.0;
@@ -258,7 +260,7 @@ __global__ void head_init_kernel(WsHead *h, double *hist, long long nrows, unsig
         h->cg_gamma = 0.0;
     }
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
-    for (long long k = tid; k < nrows * 6; k += gridDim.x * (long long)blockDim.x) hist[k] = nan;
+    for (long long k = tid; k < nrows * HC; k += gridDim.x * (long long)blockDim.x) hist[k] = nan;
     for (long long k = tid; k < ncnt; k += gridDim.x * (long long)blockDim.x) cnt[k] = 0u;
 }
 
@@ -406,7 +408,10 @@ int make_ctx(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, void *wor
     c.v = v;
     c.st = (cudaStream_t)stream;
     c.ident = op->precond == KPL_PC_IDENTITY;
-    c.sigma = c.cfg.method == KPL_M_PCG_SH ? c.cfg.shift : 0.0;
+    // sigma of the fixed-shift recurrences; pcg_var_sh passes schedule[0] here
+    // (used by the init sweep) and reads the rest of the schedule on the device
+    c.sigma = (c.cfg.method == KPL_M_PCG_SH || c.cfg.method == KPL_M_PCG_VAR_SH) ? c.cfg.shift : 0.0;
+    if (c.cfg.method == KPL_M_PCG_VAR_SH && !c.cfg.schedule) return fail(KPL_EINVAL, "pcg_var_sh needs a schedule");
     return KPL_OK;
 }
 
@@ -424,6 +429,10 @@ int kind_phase(int kind, int &phase, int &pred) {
     case KPL_SW_RR_W: phase = PH_NONE; pred = PRED_FIRE; return KPL_OK;
     case KPL_SW_RR_S: phase = PH_NONE; pred = PRED_FIRE; return KPL_OK;
     case KPL_SW_RR_Z: phase = PH_RRFINAL; pred = PRED_FIRE; return KPL_OK;
+    case KPL_SW_GAP_F: phase = PH_GAPF; pred = PRED_ROW; return KPL_OK;
+    case KPL_SW_GAP_G: phase = PH_GAPG; pred = PRED_ROW; return KPL_OK;
+    case KPL_SW_GAP_H: phase = PH_GAPH; pred = PRED_ROW; return KPL_OK;
+    case KPL_SW_GAP_J: phase = PH_GAPJ; pred = PRED_ROW; return KPL_OK;
     default: return fail(KPL_EINVAL, "unknown sweep kind");
     }
 }
@@ -483,9 +492,22 @@ int do_sweep(const Ctx &c, int kind, long long row) {
                       row, c.st);
     }
     case KPL_SW_ITER:                    // the fused pipelined iteration (:408-421 + :388-390)
+        if (c.cfg.method == KPL_M_PCG_VAR_SH)
+            return with_pc(op, [&](auto pc) -> int {
+                constexpr int PC = decltype(pc)::value;
+                BodyPcgIter<PC, true> body;
+                body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
+                body.s = v->s; body.t = v->t; body.p = v->p; body.w0 = v->w0; body.w1 = v->w1;
+                body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = 0.0; body.dsig = 0.0;
+                body.schedule = c.cfg.schedule; body.want_xi = 0;
+                body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
+                return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred, row,
+                              c.st);
+            });
         return with_pc(op, [&](auto pc) -> int {
             constexpr int PC = decltype(pc)::value;
             BodyPcgIter<PC> body;
+            body.schedule = nullptr; body.dsig = 0.0;
             body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
             body.s = v->s; body.t = v->t; body.p = v->p; body.w0 = v->w0; body.w1 = v->w1;
             body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = c.sigma;
@@ -534,9 +556,37 @@ int do_sweep(const Ctx &c, int kind, long long row) {
         return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, qq, qq, SEL_FIXED), rz, c.ws, c.cfg, phase, pred, row,
                       c.st);
     }
+    case KPL_SW_GAP_F: case KPL_SW_GAP_G: case KPL_SW_GAP_H: case KPL_SW_GAP_J: {
+        auto go = [&](auto body, const double *in) -> int {
+            body.b = v->b; body.r = v->r; body.t = v->t; body.s = v->s; body.z = v->z;
+            body.w0 = v->w0; body.w1 = v->w1; body.w = v->w0; body.sig = c.sigma;
+            body.schedule = c.cfg.method == KPL_M_PCG_VAR_SH ? c.cfg.schedule : nullptr;
+            return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, in, in, SEL_FIXED), body, c.ws, c.cfg, phase, pred,
+                          row, c.st);
+        };
+        if (kind == KPL_SW_GAP_F) return go(BodyGap<GAP_F>(), v->x);
+        if (kind == KPL_SW_GAP_G) return go(BodyGap<GAP_G>(), c.ident ? v->t : v->p);
+        if (kind == KPL_SW_GAP_H) return go(BodyGap<GAP_H>(), u);
+        return go(BodyGap<GAP_J>(), c.ident ? v->s : v->q);
+    }
     default:
         return fail(KPL_EINVAL, "unknown sweep kind");
     }
+}
+
+// The record-point sweeps of row j: all gap norms with track_gaps, otherwise
+// the true residual on the cadence (solvers.py:398-402, :233-234).
+int record_sweeps(const Ctx &c, long long j, bool cadence_only) {
+    int rc;
+    if (c.cfg.track_gaps) {
+        if ((rc = do_sweep(c, KPL_SW_GAP_F, j)) != KPL_OK) return rc;
+        if (c.cfg.method == KPL_M_CG) return KPL_OK;
+        for (int k : {KPL_SW_GAP_G, KPL_SW_GAP_H, KPL_SW_GAP_J})
+            if ((rc = do_sweep(c, k, j)) != KPL_OK) return rc;
+        return KPL_OK;
+    }
+    if (cadence_only && j % 10 != 0) return KPL_OK;
+    return do_sweep(c, KPL_SW_TRUE, j);
 }
 
 int head_init(const Ctx &c) {
@@ -606,7 +656,7 @@ int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v,
     if (rc != KPL_OK) return rc;
     if (op->chunks_global > 0) return fail(KPL_EINVAL, "multi-GPU operators are driven sweep by sweep");
     for (int64_t j = first; j < first + count; ++j) {
-        if (j % 10 == 0 && (rc = do_sweep(c, KPL_SW_TRUE, j)) != KPL_OK) return rc;
+        if ((rc = record_sweeps(c, j, true)) != KPL_OK) return rc;
         if (c.cfg.method == KPL_M_CG) {
             if ((rc = do_sweep(c, KPL_SW_CG_P, 0)) != KPL_OK) return rc;
             if ((rc = do_sweep(c, KPL_SW_CG_X, 0)) != KPL_OK) return rc;
@@ -629,7 +679,7 @@ int kpl_solver_cg_pass(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v,
     if (rc != KPL_OK) return rc;
     if (c.cfg.method != KPL_M_CG) return fail(KPL_EINVAL, "cg_pass is for classic CG");
     if (pass == 1) {
-        if (j % 10 == 0 && (rc = do_sweep(c, KPL_SW_TRUE, j)) != KPL_OK) return rc;
+        if ((rc = record_sweeps(c, j, true)) != KPL_OK) return rc;
         return do_sweep(c, KPL_SW_CG_P, 0);
     }
     return do_sweep(c, KPL_SW_CG_X, 0);
@@ -646,10 +696,10 @@ int kpl_solver_finish(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, 
     // the final record always carries ||b - A x|| (solvers.py:233-234, `last`);
     // the cadence produced it already iff its slot is no longer NaN
     double have = 0.0;
-    cudaMemcpyAsync(&have, c.ws.hist + 6 * s.iter + 5, sizeof(double), cudaMemcpyDeviceToHost, c.st);
+    cudaMemcpyAsync(&have, c.ws.hist + HC * s.iter + 5, sizeof(double), cudaMemcpyDeviceToHost, c.st);
     if (cudaStreamSynchronize(c.st) != cudaSuccess) return cuda_check("finish");
     if (!std::isnan(have)) return KPL_OK;
-    return do_sweep(c, KPL_SW_TRUE, s.iter);
+    return record_sweeps(c, s.iter, false);
 }
 
 int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfgp, int32_t kind, int64_t row, void *workspace,

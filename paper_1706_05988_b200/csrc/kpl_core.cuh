@@ -17,6 +17,7 @@ constexpr int NT = 256;          // threads per CTA for every sweep
 constexpr int NWARP = NT / 32;   // 8 warps
 constexpr int NQ = 4;            // reduced quantities per item (max)
 constexpr int RB = 256;          // CSR rows per item (one row per thread)
+constexpr int HC = 10;           // history columns: alpha beta gamma delta |r| true f g h j
 
 // ---------------------------------------------------------------- workspace
 // Offset 0: head (1 KiB).  Mirrors kpl_status in its first 16 int64.
@@ -43,6 +44,10 @@ enum Phase : int {
     PH_TRUE = 6,      // ||b - A x|| into the current history row
     PH_CGHEAD = 7,    // classic CG: gamma, rho -> beta, convergence, last
     PH_CGDELTA = 8,   // classic CG: delta -> alpha, record, done
+    PH_GAPF = 9,      // track_gaps: ||b - A x||, ||f|| = ||(b - A x) - r||      (solvers.py:148-149)
+    PH_GAPG = 10,     // ||axpy(-sigma_prev, t, A p) - s||                      (:153)
+    PH_GAPH = 11,     // ||axpy(-sigma_prev, r, A u) - w||                      (:152)
+    PH_GAPJ = 12,     // ||A q - z||                                            (:154)
 };
 
 // Launch predicate evaluated uniformly by every CTA at kernel start.
@@ -67,7 +72,7 @@ struct Ws {                   // device view of the caller's workspace
     double *items;            // [items][NQ]
     double *chunks;           // [chunks_global][NQ] (global table)
     unsigned int *chunk_cnt;  // [nch_local]
-    double *hist;             // [max_iters+1][6]
+    double *hist;             // [max_iters+1][HC]
     long long *reps;          // [max_iters+1]
     long long chunk_offset;   // first global chunk of this rank
     long long chunks_global;
@@ -76,8 +81,10 @@ struct Ws {                   // device view of the caller's workspace
 
 struct Cfg {                  // scalar view of kpl_cfg
     int method;
+    int track_gaps;
     double shift, rtol, tau, coef;
     long long max_iters;
+    const double *schedule;   // pcg_var_sh: shift_schedule on the device (max_iters+1 values)
 };
 
 // ------------------------------------------------------------- memory ops
@@ -222,7 +229,7 @@ __device__ bool pipelined_scalars(WsHead *h, long long i, double gamma, double d
     return true;
 }
 
-__device__ __forceinline__ double *hist_row(const Ws &ws, long long i) { return ws.hist + 6 * i; }
+__device__ __forceinline__ double *hist_row(const Ws &ws, long long i) { return ws.hist + HC * i; }
 
 __device__ __forceinline__ bool converged_test(const Cfg &cfg, const WsHead *h, double rnorm) {
     // solvers.py:391
@@ -313,6 +320,19 @@ __device__ void finalize(const Ws &ws, const Cfg &cfg, int phase, const double (
     }
     case PH_TRUE:
         hist_row(ws, h->iter)[5] = sqrt(v[0]);
+        break;
+    case PH_GAPF:
+        hist_row(ws, h->iter)[5] = sqrt(v[0]);
+        hist_row(ws, h->iter)[6] = sqrt(v[1]);
+        break;
+    case PH_GAPG:
+        hist_row(ws, h->iter)[7] = sqrt(v[0]);
+        break;
+    case PH_GAPH:
+        hist_row(ws, h->iter)[8] = sqrt(v[0]);
+        break;
+    case PH_GAPJ:
+        hist_row(ws, h->iter)[9] = sqrt(v[0]);
         break;
     case PH_CGHEAD: {
         // v = {(r,u), (r,r)} of the updated vectors: row i = iter + 1 (solvers.py:258-268)

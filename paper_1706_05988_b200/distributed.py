@@ -21,19 +21,17 @@ one process on one device (exchanges and gathers become device copies; all
 sweeps are launched sequentially, none waits on another) -- the single-GPU
 stand-in used by the parity tests.
 
-Scope: stencil operators, identity or constant-diagonal Jacobi, methods
-cg / pcg / pcg_sh / pcg_rr.  Row-block CSR with general halo gathers is not
-built yet (raises NotImplementedError).
+Scope: stencil operators, identity or constant-diagonal Jacobi, every method
+(cg / pcg / pcg_sh / pcg_var_sh / pcg_rr) and track_gaps.  Row-block CSR with
+general halo gathers is not built yet (raises NotImplementedError).
 """
 
 from __future__ import annotations
 
-import math
-
 import numpy as np
 
 from . import _lib, device as D
-from .solvers import (BreakdownError, IterationRecord, SolveResult, SolverConfig, _CODE)
+from .solvers import (HC, BreakdownError, SolveResult, SolverConfig, make_kcfg, records_from)
 
 _ZC_CHOICES = (16, 8, 4, 2, 1)
 
@@ -70,7 +68,7 @@ class _RankState:
 
     VEC_NAMES = ("x", "r", "u", "w0", "w1", "z", "q", "s", "t", "p", "p1")
 
-    def __init__(self, plan: SlabPlan, rank, diag, pc_code, pc_const, cfg: SolverConfig, device):
+    def __init__(self, plan: SlabPlan, rank, diag, pc_code, pc_const, cfg: SolverConfig, device, kcfg):
         t = D.torch()
         self.plan, self.rank, self.device = plan, rank, device
         self.cfg = cfg
@@ -112,13 +110,7 @@ class _RankState:
         op.chunks_global = plan.chunks_global
         self.op = op
 
-        c = _lib.KplCfg()
-        c.method = _CODE[cfg.method]
-        c.shift = float(cfg.shift)
-        c.max_iters = int(cfg.max_iters)
-        c.rtol = float(cfg.rtol)
-        c.rr_threshold = float(cfg.rr_threshold)
-        self.kcfg = c
+        self.kcfg = kcfg
 
         v = _lib.KplVecs()
         for nm in self.VEC_NAMES:
@@ -171,8 +163,8 @@ class _RankState:
 
     def history(self, rows):
         t = D.torch()
-        raw = self.ws[self.hist_off:self.hist_off + 48 * rows]
-        return raw.view(t.float64).reshape(rows, 6).cpu().numpy()
+        raw = self.ws[self.hist_off:self.hist_off + 8 * HC * rows]
+        return raw.view(t.float64).reshape(rows, HC).cpu().numpy()
 
 
 class LocalComm:
@@ -243,8 +235,6 @@ class DistributedStencilSolve:
     def __init__(self, A, M, cfg: SolverConfig, comm, zc=0):
         if not hasattr(A, "stencil_spec"):
             raise NotImplementedError("multi-GPU row-block CSR (general halo gather) is not built yet")
-        if cfg.track_gaps or cfg.method == "pcg_var_sh":
-            raise NotImplementedError("track_gaps / pcg_var_sh are not on the device path yet")
         self.device = D.require_cuda()
         NX, NY, NZ, diag = A.stencil_spec()
         self.A, self.cfg, self.comm = A, cfg, comm
@@ -262,12 +252,9 @@ class DistributedStencilSolve:
             pc = _lib.KPL_PC_JACOBI_CONST
         else:
             raise NotImplementedError(f"preconditioner {kind!r} not on the device path")
-        self.states = [_RankState(self.plan, r, diag, pc, c, cfg, self.device)
+        self.kcfg, self._keep = make_kcfg(cfg, A, self, self.device)
+        self.states = [_RankState(self.plan, r, diag, pc, c, cfg, self.device, self.kcfg)
                        for r in comm.local_ranks()]
-        if cfg.method == "pcg_rr":
-            coef = (A.mu * math.sqrt(A.n) + 1.0) * A.norm_inf()
-            for s in self.states:
-                s.kcfg.rr_coef = coef
         self.limit = cfg.max_iters + (1 if cfg.method == "cg" else 0)
 
     # -- collective building blocks
@@ -313,8 +300,7 @@ class DistributedStencilSolve:
         """One iteration (host index j = self.issued)."""
         j = self.issued
         m = self.cfg.method
-        if j % 10 == 0:
-            self.sweep(_lib.KPL_SW_TRUE, row=j, inputs=("x",))
+        self.record(j, cadence_only=True)
         if m == "cg":
             par = "p1" if (j & 1) else "p"
             self.sweep(_lib.KPL_SW_CG_P, inputs=(par, "u"))
@@ -327,6 +313,18 @@ class DistributedStencilSolve:
                 self.sweep(_lib.KPL_SW_RR_S, inputs=("p",))
                 self.sweep(_lib.KPL_SW_RR_Z, inputs=("q",))
         self.issued += 1
+
+    def record(self, j, cadence_only):
+        """Record-point sweeps of row j (solvers.py:398-402): gap norms with
+        track_gaps, else the true residual on the i % 10 cadence."""
+        if self.cfg.track_gaps:
+            self.sweep(_lib.KPL_SW_GAP_F, row=j, inputs=("x",))
+            if self.cfg.method != "cg":
+                self.sweep(_lib.KPL_SW_GAP_G, row=j, inputs=("p",))
+                self.sweep(_lib.KPL_SW_GAP_H, row=j, inputs=("u",))
+                self.sweep(_lib.KPL_SW_GAP_J, row=j, inputs=("q",))
+        elif not cadence_only or j % 10 == 0:
+            self.sweep(_lib.KPL_SW_TRUE, row=j, inputs=("x",))
 
     def run(self, poll=16):
         self.init()
@@ -347,11 +345,8 @@ class DistributedStencilSolve:
             raise _lib.KplError(f"distributed solve ended in state {st.state}")
         rows = int(st.iter) + 1
         if np.isnan(s0.history(rows)[-1, 5]):
-            self.sweep(_lib.KPL_SW_TRUE, row=int(st.iter), inputs=("x",))
-        h = s0.history(rows)
-        history = [IterationRecord(i, *(float(c) for c in h[i, :5]),
-                                   rnorm_true=None if np.isnan(h[i, 5]) else float(h[i, 5]))
-                   for i in range(rows)]
+            self.record(int(st.iter), cadence_only=False)
+        history = records_from(s0.history(rows), rows)
         reps = []
         if st.n_replacements:
             t = D.torch()

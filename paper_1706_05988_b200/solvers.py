@@ -34,7 +34,44 @@ UNIT_ROUNDOFF = float(np.finfo(np.float64).eps) / 2.0
 DEFAULT_RR_THRESHOLD = math.sqrt(UNIT_ROUNDOFF)          # solvers.py:46
 _METHODS = ("cg", "pcg", "pcg_sh", "pcg_var_sh", "pcg_rr")
 _CODE = {"cg": _lib.KPL_M_CG, "pcg": _lib.KPL_M_PCG, "pcg_sh": _lib.KPL_M_PCG_SH,
-         "pcg_rr": _lib.KPL_M_PCG_RR}
+         "pcg_var_sh": _lib.KPL_M_PCG_VAR_SH, "pcg_rr": _lib.KPL_M_PCG_RR}
+HC = _lib.KPL_HIST_COLS
+
+
+def records_from(h, rows):
+    """Device history table [rows, 10] -> IterationRecord list (NaN -> None)."""
+    opt = lambda v: None if np.isnan(v) else float(v)
+    return [IterationRecord(i, *(float(c) for c in h[i, :5]), rnorm_true=opt(h[i, 5]),
+                            gap_f=opt(h[i, 6]), gap_g=opt(h[i, 7]), gap_h=opt(h[i, 8]),
+                            gap_j=opt(h[i, 9]))
+            for i in range(rows)]
+
+
+def make_kcfg(cfg, A, dm, device):
+    """kpl_cfg for `cfg`; returns (kcfg, keep-alive tensors)."""
+    c = _lib.KplCfg()
+    c.method = _CODE[cfg.method]
+    c.track_gaps = 1 if cfg.track_gaps else 0
+    c.shift = float(cfg.shift)
+    c.max_iters = int(cfg.max_iters)
+    c.rtol = float(cfg.rtol)
+    c.rr_threshold = float(cfg.rr_threshold)
+    keep = []
+    if cfg.method == "pcg_rr":
+        # _ReplacementTrigger.coef = (mu*sqrt(n) + 1) * ||A||_inf (solvers.py:514)
+        if getattr(dm, "rr_coef", None) is None:
+            dm.rr_coef = (A.mu * math.sqrt(A.n) + 1.0) * A.norm_inf()
+        c.rr_coef = dm.rr_coef
+    if cfg.method == "pcg_var_sh":
+        sched = np.asarray(cfg.shift_schedule, dtype=np.float64)
+        if sched.ndim != 1 or len(sched) < cfg.max_iters + 1:
+            raise ValueError("shift schedule must provide max_iters + 1 values")   # solvers.py:439-440
+        t = D.torch()
+        dsched = t.from_numpy(np.ascontiguousarray(sched[:cfg.max_iters + 1])).to(device)
+        keep.append(dsched)
+        c.shift_schedule = dsched.data_ptr()
+        c.shift = float(sched[0])
+    return c, keep
 
 
 class BreakdownError(ArithmeticError):
@@ -127,12 +164,6 @@ class _Solve:
     """One solve: device vectors, workspace, and the host enqueue loop."""
 
     def __init__(self, A, M, b, x0, cfg: SolverConfig, *, zc=0, vx=0, chunk_blocks=0):
-        if cfg.track_gaps:
-            raise NotImplementedError(
-                "track_gaps (gap instrumentation, solvers.py:142-167) is not on the device path "
-                "yet (SURVEY.md 8f-1)")
-        if cfg.method == "pcg_var_sh":
-            raise NotImplementedError("pcg_var_sh (solvers.py:425-498) is not on the device path yet")
         self.device = dev = D.require_cuda()
         t = D.torch()
         self.cfg = cfg
@@ -145,19 +176,7 @@ class _Solve:
         if x0 is not None:
             self.x0, _ = D.to_device_f64(x0, n, dev, "initial guess")
         self.op = D.make_op(self.dm, self.dp, zc=zc, vx=vx, chunk_blocks=chunk_blocks)
-        c = _lib.KplCfg()
-        c.method = _CODE[cfg.method]
-        c.shift = float(cfg.shift)
-        c.max_iters = int(cfg.max_iters)
-        c.rtol = float(cfg.rtol)
-        c.rr_threshold = float(cfg.rr_threshold)
-        if cfg.method == "pcg_rr":
-            # _ReplacementTrigger.coef = (mu*sqrt(n) + 1) * ||A||_inf (solvers.py:514)
-            dm = self.dm
-            if getattr(dm, "rr_coef", None) is None:
-                dm.rr_coef = (A.mu * math.sqrt(A.n) + 1.0) * A.norm_inf()
-            c.rr_coef = dm.rr_coef
-        self.kcfg = c
+        self.kcfg, self._keep = make_kcfg(cfg, A, self.dm, dev)
         ident = self.dp.identity
         f64 = dict(dtype=t.float64, device=dev)
         emp = lambda: t.empty(n, **f64)
@@ -258,8 +277,8 @@ class _Solve:
 
     def history_array(self, rows):
         t = D.torch()
-        raw = self.ws[self.hist_off:self.hist_off + 48 * rows]
-        return raw.view(t.float64).reshape(rows, 6).cpu().numpy()
+        raw = self.ws[self.hist_off:self.hist_off + 8 * HC * rows]
+        return raw.view(t.float64).reshape(rows, HC).cpu().numpy()
 
     def result(self):
         st = self.read_status()
@@ -270,10 +289,7 @@ class _Solve:
         self.finish()
         st = self.read_status()
         iters = int(st.iter)
-        h = self.history_array(iters + 1)
-        history = [IterationRecord(i, *(float(c) for c in h[i, :5]),
-                                   rnorm_true=None if np.isnan(h[i, 5]) else float(h[i, 5]))
-                   for i in range(iters + 1)]
+        history = records_from(self.history_array(iters + 1), iters + 1)
         reps = []
         if st.n_replacements:
             t = D.torch()
@@ -298,7 +314,11 @@ class _Solve:
             return
         h = self.history_array(i + 1)[i]
         host = lambda v: None if v is None else v.cpu().numpy().copy()
-        sig = float(self.cfg.shift) if self.cfg.method == "pcg_sh" else 0.0
+        sig = sig_cur = float(self.cfg.shift) if self.cfg.method == "pcg_sh" else 0.0
+        if self.cfg.method == "pcg_var_sh":
+            sched = self.cfg.shift_schedule
+            sig = float(sched[i])
+            sig_cur = float(sched[i + 1]) if i + 1 < len(sched) else None
         if self.cfg.method == "cg":
             par = (i + 1) & 1      # p written by pass 1 of row i
             state = SolverState(i, host(self.x), host(self.r), host(self.u), *map(float, h[:4]),
@@ -308,7 +328,7 @@ class _Solve:
             state = SolverState(i, host(self.x), host(self.r), host(self.u), *map(float, h[:4]),
                                 w=host(w), s_prev=host(self.s), t_prev=host(self.t),
                                 p_prev=host(self.p), q_prev=host(self.q), z_prev=host(self.z),
-                                sigma_prev=sig, sigma=sig)
+                                sigma_prev=sig, sigma=sig_cur)
         callback(state)
 
 
@@ -337,7 +357,7 @@ def solve_pcg_rr(A, M, b, x0, cfg: SolverConfig, callback=None) -> SolveResult:
 
 
 def solve_pcg_var_shifted(A, M, b, x0, cfg: SolverConfig, callback=None) -> SolveResult:
-    """Variable-shift p-CG (solvers.py:425-498): not on the device path yet."""
+    """Variable-shift p-CG, Alg. 4 (solvers.py:425-498) on the device."""
     return _solve(A, M, b, x0, _as(cfg, "pcg_var_sh"), callback)
 
 

@@ -69,3 +69,11 @@ def first_diff(a, b):
         return "equal"
     idx = tuple(x[0] for x in bad)
     return f"first mismatch at {idx}: {a[idx]!r} vs {b[idx]!r}"
+
+
+def hist11(res):
+    """All IterationRecord fields (gaps included), NaN for None."""
+    f = lambda v: np.nan if v is None else v
+    return np.array([[r.iter, r.alpha, r.beta, r.gamma, r.delta, r.rnorm_recursive,
+                      f(r.rnorm_true), f(r.gap_f), f(r.gap_g), f(r.gap_h), f(r.gap_j)]
+                     for r in res.history], dtype=np.float64)

@@ -175,3 +175,24 @@ def test_local_ranks_bitwise_2d_jacobi(P):
     assert res.iterations == ref.iterations and res.converged
     assert [r.alpha for r in res.history] == [r.alpha for r in ref.history]
     assert x.tobytes() == ref.x.tobytes()
+
+
+@gpu
+@pytest.mark.parametrize("method,extra", [("pcg_sh", {"shift": 1.0}),
+                                          ("pcg_var_sh", {"shift_schedule": tuple(0.05 * k for k in range(41))})])
+def test_local_ranks_gaps_bitwise(method, extra):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200.distributed import LocalComm, SlabPlan, solve_distributed
+    A = K.Stencil3D(64, 16, 16)
+    b = np.full(A.n, 1 / math.sqrt(A.n))
+    cfg = K.SolverConfig(method=method, max_iters=40, track_gaps=True, **extra)
+    ref = _one_gpu(A, None, b, cfg, 4)
+    plan = SlabPlan(64, 16, 16, 2, 4)
+    res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(2)], None, cfg,
+                            comm=LocalComm(2), zc=4)
+    for a, c in zip(res.history, ref.history):
+        assert (a.gap_f, a.gap_g, a.gap_h, a.gap_j, a.rnorm_true) == \
+               (c.gap_f, c.gap_g, c.gap_h, c.gap_j, c.rnorm_true)
+        assert (a.alpha, a.beta) == (c.alpha, c.beta)

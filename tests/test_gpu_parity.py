@@ -279,3 +279,63 @@ def test_tma_and_register_sweeps_identical(monkeypatch):
     monkeypatch.setenv("KPL_NO_TMA", "1")
     r2 = K.solve(A, None, b, None, cfg)
     assert same_bits(hist6(r1), hist6(r2)) and same_bits(r1.x, r2.x)
+
+
+# ------------------------------------------------- 8f-1: gaps, variable shift
+
+from gpu_helpers import hist11  # noqa: E402
+
+
+def run_both11(A, b, cfg_kw):
+    res = K.solve(A, None, b, None, K.SolverConfig(**cfg_kw))
+    ores = O.solve(A, None, b, None, O.Config(**cfg_kw), dot=gpu_dot(A))
+    h, oh = hist11(res), np.ascontiguousarray(ores.history)
+    assert same_bits(h, oh), first_diff(h, oh)
+    assert same_bits(res.x, ores.x)
+    return res
+
+
+@pytest.mark.parametrize("m,extra", [("cg", {}), ("pcg", {}), ("pcg_sh", {"shift": 0.9}),
+                                     ("pcg_var_sh", {"shift_schedule": tuple(0.1 * k for k in range(62))}),
+                                     ("pcg_rr", {})])
+def test_track_gaps_bitwise(m, extra):
+    """gap_f/g/h/j and the true residual at every record (solvers.py:142-167)."""
+    A = K.random_spd(48, cond=1e3, seed=21)
+    b = O.spmv(O.as_oracle_operator(A), np.full(48, 1 / math.sqrt(48.0)))
+    run_both11(A, b, dict(method=m, max_iters=60, rtol=0.0, track_gaps=True, **extra))
+
+
+@pytest.mark.parametrize("A", [K.Stencil2D(5, 4), K.Stencil3D(24, 18, 20)])
+def test_track_gaps_stencil_bitwise(A):
+    b = np.full(A.n, 1 / math.sqrt(A.n))
+    res = run_both11(A, b, dict(method="pcg_sh", shift=1.0, max_iters=30, track_gaps=True))
+    first = res.history[0]
+    assert first.gap_f == 0.0 and first.gap_g == 0.0 and first.gap_j == 0.0   # test_solvers.py:148-159
+
+
+def test_var_shift_ramp_bitwise():
+    """Alg. 4 (solvers.py:425-498) with a ramped schedule (test_acceptance.py:398-409 shape)."""
+    A = K.Stencil2D(60, 50)
+    b = np.full(A.n, 1 / math.sqrt(A.n))
+    sched = (0.0,) + tuple(4.0 * min(1.0, i / 50.0) for i in range(300))
+    run_both11(A, b, dict(method="pcg_var_sh", shift_schedule=sched, max_iters=300))
+
+
+def test_var_shift_constant_equals_pcg_sh():
+    A = K.Stencil3D(20, 16, 12)
+    b = np.full(A.n, 1 / math.sqrt(A.n))
+    sh = K.solve(A, None, b, None, K.SolverConfig(method="pcg_sh", shift=0.7, max_iters=80))
+    var = K.solve(A, None, b, None, K.SolverConfig(method="pcg_var_sh", shift_schedule=(0.7,) * 81,
+                                                    max_iters=80))
+    assert same_bits(hist11(sh), hist11(var)) and same_bits(sh.x, var.x)
+
+
+def test_var_shift_jacobi_csr_bitwise():
+    A = problems.varcoef_3d(8, seed=0)
+    b = np.random.default_rng(1).standard_normal(A.n)
+    sched = tuple(0.1 + 0.002 * k for k in range(401))
+    cfg = dict(method="pcg_var_sh", shift_schedule=sched, max_iters=400, rtol=1e-12)
+    res = K.solve(A, K.make_jacobi(A), b, None, K.SolverConfig(**cfg))
+    oA = O.as_oracle_operator(A)
+    ores = O.solve(oA, O.make_jacobi(oA), b, None, O.Config(**cfg), dot=gpu_dot(A))
+    assert same_bits(hist11(res), np.ascontiguousarray(ores.history)) and same_bits(res.x, ores.x)
