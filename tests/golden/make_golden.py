@@ -197,9 +197,40 @@ def jacobi_and_3d():
     np.savez_compressed(os.path.join(HERE, "jacobi_3d.npz"), **out)
 
 
+def shift_selection():
+    """stability.py sweep + shift_study.py:46-51 margin rule on reference histories."""
+    from kpl import CoefficientHistory, default_sigma_grid, select_shift
+    out = {}
+    cases = []
+    A = laplacian_2d(200, 200)
+    b = spmv(A, np.full(A.n, 1.0 / np.sqrt(A.n)))
+    cases.append(("cfg1", A, None, b, 2000, 1e-12))
+    Aj = laplacian_2d(64, 48)
+    Mj = make_jacobi(Aj)
+    bj = spmv(Aj, np.random.default_rng(0).random(Aj.n))
+    cases.append(("j2d", Aj, Mj, bj, 1000, 1e-10))
+    for tag, A_, M_, b_, maxit, rtol in cases:
+        base = solve(A_, M_, b_, None, SolverConfig(method="pcg", max_iters=maxit, rtol=rtol))
+        hist = CoefficientHistory.from_result(base)
+        grid = default_sigma_grid(A_, M_)
+        sw = select_shift(hist, base.iterations, grid)
+        floor = 4.0 * sw.psi_values.min()
+        chosen = float(sw.grid[np.argmax(sw.psi_values <= floor)])
+        out[f"{tag}_alphas"] = hist.alphas
+        out[f"{tag}_betas"] = hist.betas
+        out[f"{tag}_i"] = np.int64(base.iterations)
+        out[f"{tag}_grid"] = grid
+        out[f"{tag}_psi"] = sw.psi_values
+        out[f"{tag}_argmin"] = np.float64(sw.argmin)
+        out[f"{tag}_chosen"] = np.float64(chosen)
+        print(f"  {tag}: i={base.iterations} argmin={sw.argmin} chosen={chosen!r}")
+    np.savez_compressed(os.path.join(HERE, "shift.npz"), **out)
+
+
 if __name__ == "__main__":
     print("reference kpl", kpl.__version__, "from", kpl.__file__)
-    kernels()
-    solvers_small()
-    config1()
-    jacobi_and_3d()
+    only = sys.argv[1:]
+    for name, fn in (("kernels", kernels), ("solvers_small", solvers_small), ("config1", config1),
+                     ("jacobi_3d", jacobi_and_3d), ("shift", shift_selection)):
+        if not only or name in only:
+            fn()
