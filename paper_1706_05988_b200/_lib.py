@@ -12,7 +12,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libkpl_b200.so")
+LIB_PATH = os.environ.get("KPL_LIB") or os.path.join(HERE, "lib", "libkpl_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "kpl_b200.h")
 
 # constants mirrored from include/kpl_b200.h

@@ -73,7 +73,8 @@ int make_layout(const kpl_op *op, Layout &L) {
         if (op->row_ptr && ((!op->col_idx && op->nnz) || (!op->values && op->nnz)))
             return fail(KPL_EINVAL, "CSR arrays missing");
         const long long blocks = cdiv(op->n, RB);
-        const int cb = op->chunk_blocks > 0 ? op->chunk_blocks : 16;
+        const int cb = op->chunk_blocks > 0 ? op->chunk_blocks : 8;
+        if (cb > 64) return fail(KPL_EINVAL, "chunk_blocks must be <= 64");
         L.vx = 1; L.wx = NWARP; L.wy = 1; L.zc = cb;
         L.T = cb;
         L.items = blocks;
@@ -83,7 +84,7 @@ int make_layout(const kpl_op *op, Layout &L) {
     return fail(KPL_EINVAL, "unknown operator kind");
 }
 
-struct Offsets { long long items, chunks, cnt, hist, reps, total; };
+struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, total; };
 
 Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     Offsets o;
@@ -93,7 +94,8 @@ Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     o.cnt = o.chunks + align256(8LL * NQ * cg);
     o.hist = o.cnt + align256(4LL * L.nch);
     o.reps = o.hist + align256(8LL * HC * (max_iters + 1));
-    o.total = o.reps + align256(8LL * (max_iters + 1));
+    o.nbuf = o.reps + align256(8LL * (max_iters + 1));
+    o.total = o.nbuf + (op->kind == KPL_OP_CSR && op->row_ptr ? align256(8LL * op->n) : 0);
     return o;
 }
 
@@ -107,6 +109,7 @@ Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspa
     ws.chunk_cnt = reinterpret_cast<unsigned int *>(base + o.cnt);
     ws.hist = reinterpret_cast<double *>(base + o.hist);
     ws.reps = reinterpret_cast<long long *>(base + o.reps);
+    ws.nbuf = reinterpret_cast<double *>(base + o.nbuf);
     ws.chunk_offset = op->chunks_global > 0 ? op->chunk_offset : 0;
     ws.chunks_global = op->chunks_global > 0 ? op->chunks_global : L.nch;
     ws.inline_final = op->chunks_global > 0 ? 0 : 1;
@@ -139,8 +142,14 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
         else
             stencil_sweep<1, In, Body><<<(unsigned)L.items, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
     } else {
+        // split CSR: high-occupancy SpMV into the workspace, then the chunk sweep
         CGeo g{op->n, op->row_ptr, op->col_idx, op->values};
-        csr_sweep<In, Body><<<(unsigned)L.items, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
+        if constexpr (Body::kStencil) {
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            csr_spmv_kernel<In><<<(unsigned)L.items, NT, 0, st>>>(g, in, ws.nbuf, ws, pred, row);
+        }
+        csr_chunk_sweep<In, Body><<<(unsigned)L.nch, NT, 0, st>>>(g, L, in, body, ws.nbuf, ws, cfg, phase, pred,
+                                                                 row);
     }
     return cuda_check("sweep launch");
 }
@@ -340,6 +349,13 @@ int kpl_spmv(const kpl_op *op, const double *v, double *out, void *stream) {
     BodySpmv body;
     body.out = out;
     InVec<KPL_PC_IDENTITY> in = in_vec<KPL_PC_IDENTITY>(op, v, v, SEL_FIXED);
+    if (op->kind == KPL_OP_CSR) {
+        CGeo g{op->n, op->row_ptr, op->col_idx, op->values};
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        csr_spmv_kernel<InVec<KPL_PC_IDENTITY>><<<(unsigned)L.items, NT, 0, (cudaStream_t)stream>>>(
+            g, in, out, ws, PRED_ALWAYS, 0);
+        return cuda_check("spmv launch");
+    }
     return launch(op, L, in, body, ws, cfg, PH_NONE, PRED_ALWAYS, 0, (cudaStream_t)stream);
 }
 

@@ -74,6 +74,7 @@ struct Ws {                   // device view of the caller's workspace
     unsigned int *chunk_cnt;  // [nch_local]
     double *hist;             // [max_iters+1][HC]
     long long *reps;          // [max_iters+1]
+    double *nbuf;             // CSR: n = A m of the current sweep (split SpMV / update)
     long long chunk_offset;   // first global chunk of this rank
     long long chunks_global;
     int inline_final;         // 1: last CTA finalises (single GPU)

@@ -286,6 +286,153 @@ csr_sweep(CGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pre
     }
 }
 
+// ---------------------------------------------------------------------------
+// CSR, split form (the production CSR path).
+//
+//  csr_spmv_kernel   n = A * xf(input): one CTA per 256-row block, the block's
+//                    nonzeros staged through shared memory (coalesced
+//                    col_idx/values loads, gathered input, products), each
+//                    thread summing its row left to right from +0.0 -- the
+//                    reference csr_matvec order.  No reductions, small register
+//                    and smem footprint -> high occupancy for the gathers.
+//  csr_chunk_sweep   one CTA per reduction chunk (chunk_blocks 256-row items):
+//                    the body's update for every row of the chunk with n read
+//                    back from memory, item partials kept in shared memory, the
+//                    chunk fold (level 3) done in-CTA, one completion atomic per
+//                    chunk.  Same items, same tree: bit-identical to csr_sweep.
+template <class In>
+__global__ void __launch_bounds__(NT, 6)
+csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
+    constexpr int PER = CSR_WIN / NT;
+    __shared__ double sprod[CSR_WIN];
+    if (ws.head && !pred_ok(ws.head, pred, row)) return;
+    if (ws.head) in.setup(ws);
+    const int tid = threadIdx.x;
+    const long long r0 = (long long)blockIdx.x * RB;
+    const long long r = r0 + tid;
+    const bool ok = r < g.n;
+    const long long rend = min(r0 + RB, g.n);
+    const long long k0 = __ldg(g.row_ptr + r0), k1 = __ldg(g.row_ptr + rend);
+    long long lo = 0, hi = 0;
+    if (ok) { lo = __ldg(g.row_ptr + r); hi = __ldg(g.row_ptr + r + 1); }
+    double a = 0.0;
+    for (long long wk = k0; wk < k1; wk += CSR_WIN) {
+        const long long we = min(wk + (long long)CSR_WIN, k1);
+        int col[PER];
+        double val[PER], raw[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const long long kk = wk + tid + (long long)j * NT;
+            col[j] = 0; val[j] = 0.0;
+            if (kk < we) { col[j] = __ldcs(g.col_idx + kk); val[j] = __ldcs(g.values + kk); }
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const long long kk = wk + tid + (long long)j * NT;
+            raw[j] = 0.0;
+            if (kk < we) { double t[1]; in.template raw<1>(in.base(), col[j], t); raw[j] = t[0]; }
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const long long kk = wk + tid + (long long)j * NT;
+            if (kk < we) sprod[kk - wk] = __dmul_rn(val[j], in.xf(raw[j], col[j]));
+        }
+        __syncthreads();
+        const long long a0 = max(lo, wk), a1 = min(hi, we);
+        for (long long kk = a0; kk < a1; ++kk) a = __dadd_rn(a, sprod[kk - wk]);   // csr_matvec order
+        __syncthreads();
+    }
+    if (ok) out[r] = a;
+}
+
+template <class In, class Body>
+__global__ void __launch_bounds__(NT, 3)
+csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ nin, Ws ws, Cfg cfg, int phase,
+                int pred, long long row) {
+    constexpr int Q = Body::NQ;
+    __shared__ double sred[NQ * NWARP];
+    __shared__ double sitem[Q > 0 ? Q : 1][64];
+    if (!pred_ok(ws.head, pred, row)) return;
+    body.setup(ws);
+    in.setup(ws);
+    const int tid = threadIdx.x;
+    const long long chunk = blockIdx.x;
+    const long long it0 = chunk * L.T;
+    const int nit = (int)min((long long)L.T, L.items - it0);
+    // software pipeline over the chunk's items: streams of item i+1 in flight while i computes
+    typename Body::template Regs<1> R, Rn;
+    double nn = 0.0, cen = 0.0, nn_n = 0.0, cen_n = 0.0;
+    auto fetch = [&](long long item, typename Body::template Regs<1> &RR, double &n1, double &c1) {
+        const long long r = item * RB + tid;
+        if (r < g.n) {
+            body.template load<1>(r, RR);
+            if constexpr (Body::kStencil) {
+                n1 = __ldcs(nin + r);
+                double t[1];
+                in.template raw<1>(in.base(), r, t);
+                c1 = t[0];
+            }
+        }
+    };
+    fetch(it0, R, nn, cen);
+    for (int i = 0; i < nit; ++i) {
+        const long long item = it0 + i;
+        if (i + 1 < nit) fetch(item + 1, Rn, nn_n, cen_n);
+        const long long r = item * RB + tid;
+        double acc[Q > 0 ? Q : 1][1];
+#pragma unroll
+        for (int q = 0; q < (Q > 0 ? Q : 1); ++q) acc[q][0] = 0.0;
+        if (r < g.n) {
+            const double n1[1] = {nn}, c1[1] = {cen};
+            body.template compute<1>(r, R, n1, c1, acc);
+        }
+        if constexpr (Q > 0) {
+            double t[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) t[q] = acc[q][0];
+            block_sum<Q>(t, sred);                    // item partial (levels 2b, 2c)
+            if (tid == 0) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) { sitem[q][i] = t[q]; ws.items[item * NQ + q] = t[q]; }
+            }
+        }
+        R = Rn; nn = nn_n; cen = cen_n;
+    }
+    if constexpr (Q > 0) {
+        __syncthreads();
+        // level 3 in-CTA: thread t adds items t, t+256, ... (nit <= 64) then block_sum
+        double v[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) v[q] = (tid < nit) ? __dadd_rn(0.0, sitem[q][tid]) : 0.0;
+        block_sum<Q>(v, sred);
+        __shared__ int s_last;
+        const long long cg = ws.chunk_offset + chunk;
+        if (tid == 0) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) ws.chunks[cg * NQ + q] = v[q];
+        }
+        if (!ws.inline_final) return;
+        if (tid == 0) {
+            __threadfence();
+            const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
+            s_last = (prev == (unsigned)(L.nch - 1));
+            if (s_last) __threadfence();
+        }
+        __syncthreads();
+        if (!s_last) return;
+        double f[Q];
+        strided_sum<Q>(ws.chunks, ws.chunks_global, NQ, f, sred);
+        if (tid == 0) {
+            double full[NQ] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int q = 0; q < Q; ++q) full[q] = f[q];
+            finalize(ws, cfg, phase, full);
+            ws.head->final_cnt = 0u;
+            __threadfence();
+        }
+    }
+}
+
 // Tiny single-CTA kernel: level-4 fold of the (gathered) chunk table + epilogue.
 __global__ void __launch_bounds__(NT) finalize_kernel(Ws ws, Cfg cfg, int phase, int pred, long long row) {
     __shared__ double sred[NQ * NWARP];
