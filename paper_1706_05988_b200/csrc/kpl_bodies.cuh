@@ -241,9 +241,11 @@ struct BodyPcgIter {
     const double *schedule;
     double dsig;
     template <int V> struct Regs { double x[V], r[V], z[V], s[V], t[V], u[V], q[V], p[V], d[V]; };
-    static constexpr int kTmaStreams = 5;                 // x, r, z, s, t (identity preconditioner)
+    // x, r, z, s, t (+ u, q, p with a constant-diagonal Jacobi)
+    static constexpr int kTmaStreams = PC == KPL_PC_IDENTITY ? 5 : 8;
     __device__ void load_tma(const double *S, int cs, Regs<2> &R) const {
         sm2(S, 0, cs, R.x); sm2(S, 1, cs, R.r); sm2(S, 2, cs, R.z); sm2(S, 3, cs, R.s); sm2(S, 4, cs, R.t);
+        if constexpr (PC != KPL_PC_IDENTITY) { sm2(S, 5, cs, R.u); sm2(S, 6, cs, R.q); sm2(S, 7, cs, R.p); }
     }
     __device__ void setup(const Ws &ws) {
         alpha = ws.head->alpha;

@@ -183,10 +183,19 @@ constexpr int kTmaDepth = 2;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
+// ring depth: 2 planes ahead for <= 5 streams (89 KB, 2 CTAs/SM); 1 ahead for
+// the 8-stream Jacobi update (86 KB, 2 CTAs/SM)
 template <class Body>
+constexpr int tma_depth() { return Body::kTmaStreams > 5 ? 1 : kTmaDepth; }
+
+template <class Body, int PCIN = 0>
 void tma_prepare() {
-    cudaFuncSetAttribute(tma_sweep<Body, kTmaDepth>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TmaRing<kTmaDepth, Body::kTmaStreams>::bytes());
+    cudaFuncSetAttribute(tma_sweep<Body, tma_depth<Body>(), PCIN, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TmaRing<tma_depth<Body>(), Body::kTmaStreams, false>::bytes());
+    cudaFuncSetAttribute(tma_sweep<Body, tma_depth<Body>(), PCIN, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TmaRing<tma_depth<Body>(), Body::kTmaStreams, true>::bytes());
     cudaGetLastError();
 }
 
@@ -200,8 +209,10 @@ bool tma_available() {
         cudaGetLastError();
         if (g_encode) {
             tma_prepare<BodyPcgIter<KPL_PC_IDENTITY>>();
+            tma_prepare<BodyPcgIter<KPL_PC_JACOBI_CONST>, 1>();
             tma_prepare<BodyTrue>();
             tma_prepare<BodyInitR<KPL_PC_IDENTITY>>();
+            tma_prepare<BodyInitR<KPL_PC_JACOBI_CONST>>();
             tma_prepare<BodyInitW>();
         }
     });
@@ -225,29 +236,41 @@ bool encode_box(CUtensorMap *m, const double *base, const kpl_op *op, unsigned b
 // hot kernel and its cadence/init sweeps); everything else uses the register
 // sweep of kpl_sweep.cuh.
 bool tma_eligible(const kpl_op *op, const Layout &L) {
-    return op->kind == KPL_OP_STENCIL && op->precond == KPL_PC_IDENTITY && L.vx == 2 && L.wx == 1 &&
-           L.wy == NWARP && !op->halo_lo && !op->halo_hi && op->nx % 2 == 0 && tma_available();
+    const bool shape3d = L.wx == 1 && L.wy == NWARP;             // 64 x 8 tiles
+    const bool shape2d = L.wx == NWARP && L.wy == 1 && op->ny == 1;  // 512 x 1 tiles (2D grids)
+    return op->kind == KPL_OP_STENCIL && op->precond != KPL_PC_JACOBI_VEC && L.vx == 2 &&
+           (shape3d || shape2d) && !op->halo_lo && !op->halo_hi && op->nx % 2 == 0 && tma_available();
     // (op->zhalo is supported: the stencil-input maps then cover planes -1..nz)
 }
 
 // in0/in1: stencil input (ping-pong pair or twice the same vector, wsel 0/1);
 // streams: the body's kTmaStreams plane-wise operands.
-template <class Body>
+template <class Body, int PCIN = 0>
 int launch_tma(const kpl_op *op, const Layout &L, const double *in0, const double *in1, int wsel,
                const double *const *streams, const Body &body, const Ws &ws, const Cfg &cfg, int phase,
                int pred, long long row, cudaStream_t st) {
     constexpr int NSTR = Body::kTmaStreams;
+    constexpr int DEPTH = tma_depth<Body>();
     TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     const int zext = op->zhalo ? 1 : 0;
-    bool ok = encode_box(&maps.w[0], in0, op, TMA_WX, TMA_WY, zext) &&
-              encode_box(&maps.w[1], in1, op, TMA_WX, TMA_WY, zext);
-    for (int s = 0; s < NSTR && ok; ++s) ok = encode_box(&maps.s[s], streams[s], op, TMA_TX, TMA_TY);
+    const bool two_d = L.wy == 1;
+    const unsigned wbx = two_d ? TmaShape<true>::WBX : TmaShape<false>::WBX;
+    const unsigned wby = two_d ? TmaShape<true>::WBY : TmaShape<false>::WBY;
+    const unsigned sbx = two_d ? TmaShape<true>::SBX : TmaShape<false>::SBX;
+    const unsigned sby = two_d ? TmaShape<true>::SBY : TmaShape<false>::SBY;
+    bool ok = encode_box(&maps.w[0], in0, op, wbx, wby, zext) && encode_box(&maps.w[1], in1, op, wbx, wby, zext);
+    for (int s = 0; s < NSTR && ok; ++s) ok = encode_box(&maps.s[s], streams[s], op, sbx, sby);
     if (!ok) return fail(KPL_ECUDA, "cuTensorMapEncodeTiled failed");
     SGeo g{op->nx, op->ny, op->nz, op->diag, nullptr, nullptr, op->zhalo};
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    tma_sweep<Body, kTmaDepth><<<(unsigned)L.items, NT + 32, TmaRing<kTmaDepth, NSTR>::bytes(), st>>>(
-        maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext);
+    if (two_d)
+        tma_sweep<Body, DEPTH, PCIN, true><<<(unsigned)L.items, NT + 32, TmaRing<DEPTH, NSTR, true>::bytes(), st>>>(
+            maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext, op->pc_const);
+    else
+        tma_sweep<Body, DEPTH, PCIN, false><<<(unsigned)L.items, NT + 32, TmaRing<DEPTH, NSTR, false>::bytes(),
+                                              st>>>(maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext,
+                                                    op->pc_const);
     return cuda_check("tma sweep launch");
 }
 
@@ -478,7 +501,7 @@ int do_sweep(const Ctx &c, int kind, long long row) {
             BodyInitR<PC> body;
             body.b = v->b; body.x = v->x; body.r = v->r; body.u = v->u;
             body.dinv = op->inv_diag; body.c = op->pc_const; body.copy_x = 0;
-            if constexpr (PC == KPL_PC_IDENTITY) {
+            if constexpr (PC != KPL_PC_JACOBI_VEC) {
                 if (tma) {
                     const double *streams[1] = {v->b};
                     return launch_tma(op, L, v->x, v->x, 0, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
@@ -490,7 +513,7 @@ int do_sweep(const Ctx &c, int kind, long long row) {
     case KPL_SW_INIT_W: {                // w = axpy(-sigma, r, A u) + first reductions (:376, :388-390)
         BodyInitW body;
         body.r = v->r; body.u = u; body.w = v->w0; body.sigma = c.sigma; body.ident = c.ident;
-        if (c.ident && tma) {
+        if (tma) {
             const double *streams[1] = {v->r};
             return launch_tma(op, L, u, u, 0, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
         }
@@ -533,6 +556,12 @@ int do_sweep(const Ctx &c, int kind, long long row) {
                 if (tma) {
                     const double *streams[5] = {v->x, v->r, v->z, v->s, v->t};
                     return launch_tma(op, L, v->w0, v->w1, 1, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
+                }
+            } else if constexpr (PC == KPL_PC_JACOBI_CONST) {
+                if (tma) {
+                    const double *streams[8] = {v->x, v->r, v->z, v->s, v->t, v->u, v->q, v->p};
+                    return launch_tma<BodyPcgIter<PC>, 1>(op, L, v->w0, v->w1, 1, streams, body, c.ws, c.cfg, phase,
+                                                          pred, row, c.st);
                 }
             }
             return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred, row,

@@ -26,18 +26,31 @@
 
 namespace kpl {
 
+constexpr int TMA_MAXS = 8;
 struct TmaMaps {
-    CUtensorMap w[2];      // ping-pong stencil input, box (68, 10, 1) at (x0-2, y0-1, z)
-    CUtensorMap s[5];      // x, r, z, s, t: box (64, 8, 1) at (x0, y0, z)
+    CUtensorMap w[2];            // ping-pong stencil input (w boxes, see TmaShape)
+    CUtensorMap s[TMA_MAXS];     // the body's streams (stream boxes)
 };
 
-constexpr int TMA_TX = 64, TMA_TY = 8;
-constexpr int TMA_WX = TMA_TX + 4, TMA_WY = TMA_TY + 2;       // 68 x 10
-constexpr int TMA_WPLANE = 688;                               // 68*10 = 680 doubles, padded to 128 B
-constexpr int TMA_SPLANE = TMA_TX * TMA_TY;                   // 512 doubles
-constexpr int TMA_NS = 5;
-constexpr unsigned TMA_WBYTES = TMA_WX * TMA_WY * 8;          // 5440
-constexpr unsigned TMA_SBYTES = TMA_NS * TMA_SPLANE * 8;      // 20480
+// Tile shapes.  3D grids: 64 x 8 tile, warp wy owns tile row wy; the w box
+// (68 x 10) carries the x and y halos.  2D grids (ny == 1, z = the grid's
+// rows): 512 x 1 tile, warp wx owns x-segment wx; the 516-wide halo row is
+// three 176-wide boxes, a stream row two 256-wide boxes (TMA boxes are at
+// most 256 per dimension; every copy lands 128-byte aligned).
+template <bool TWO_D> struct TmaShape;
+template <> struct TmaShape<false> {
+    static constexpr int TX = 64, TY = 8, WCOLS = 68;
+    static constexpr int WPLANE = 688;                 // 68 x 10 = 680 doubles, padded to 128 B
+    static constexpr int WBX = 68, WBY = 10, WCOPIES = 1;
+    static constexpr int SBX = 64, SBY = 8, SCOPIES = 1;
+};
+template <> struct TmaShape<true> {
+    static constexpr int TX = 512, TY = 1, WCOLS = 528;
+    static constexpr int WPLANE = 528;                 // 3 x 176 (covers x0-2 .. x0+525)
+    static constexpr int WBX = 176, WBY = 1, WCOPIES = 3;
+    static constexpr int SBX = 256, SBY = 1, SCOPIES = 2;
+};
+constexpr int TMA_SPLANE = 512;                      // both shapes: 512 doubles per stream plane
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -72,25 +85,30 @@ __device__ __forceinline__ void tma_load3d(void *dst, const CUtensorMap *map, in
         : "memory");
 }
 
-template <int D, int NSTR>
+template <int D, int NSTR, bool TWO_D = false>
 struct TmaRing {
     static constexpr int SW = D + 3, SS = D + 1;
     static constexpr size_t bytes() {
-        return (size_t)SW * TMA_WPLANE * 8 + (size_t)SS * NSTR * TMA_SPLANE * 8 + 8 * 2 * (SW + SS);
+        return (size_t)SW * TmaShape<TWO_D>::WPLANE * 8 + (size_t)SS * NSTR * TMA_SPLANE * 8 + 8 * 2 * (SW + SS);
     }
 };
 
 // Generic over bodies that declare kTmaStreams (<= 5) and load_tma(); the
 // stencil input ring is maps.w[wsel ? iter & 1 : 0].  Identity preconditioner
 // only (the stencil input is used raw).
-template <class Body, int D>
+// PCIN: transform of the stencil input -- 0 raw (m = w), 1 constant-diagonal
+// Jacobi (m = w * cin, precond.py:88-89 with inv_diag == cin).
+template <class Body, int D, int PCIN = 0, bool TWO_D = false>
 __global__ void __launch_bounds__(NT + 32, 2)
 tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws ws, Cfg cfg, int phase,
-          int pred, long long row, int wsel, int wzoff) {
+          int pred, long long row, int wsel, int wzoff, double cin) {
+    using S = TmaShape<TWO_D>;
     constexpr int NSTR = Body::kTmaStreams;
-    constexpr int SW = TmaRing<D, NSTR>::SW, SS = TmaRing<D, NSTR>::SS;
+    constexpr int SW = TmaRing<D, NSTR, TWO_D>::SW, SS = TmaRing<D, NSTR, TWO_D>::SS;
     constexpr int Q = Body::NQ > 0 ? Body::NQ : 1;
     constexpr unsigned SBYTES = NSTR * TMA_SPLANE * 8;
+    constexpr unsigned WBYTES = S::WBX * S::WBY * S::WCOPIES * 8;
+    constexpr int TMA_WPLANE = S::WPLANE;
     extern __shared__ __align__(128) unsigned char smem[];
     double *wring = reinterpret_cast<double *>(smem);
     double *sring = wring + SW * TMA_WPLANE;
@@ -109,7 +127,7 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
     const long long c = item / L.T;
     const int tile = (int)(item - c * L.T);
     const int tyi = tile / L.ntx, txi = tile - tyi * L.ntx;
-    const int x0 = txi * TMA_TX, y0 = tyi * TMA_TY;
+    const int x0 = txi * S::TX, y0 = tyi * S::TY;
     const int z0 = (int)(c * L.zc);
     const int z1 = (int)min((long long)z0 + L.zc, g.NZ);
     const int ns = z1 - z0;            // planes computed
@@ -135,8 +153,16 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
                 if (p < nw && (p <= q + 2 || q >= ns)) {
                     const int slot = p % SW;
                     if (p >= SW) mbar_wait(&wempty[slot], ((p / SW) - 1) & 1);
-                    mbar_expect_tx(&wfull[slot], TMA_WBYTES);
-                    tma_load3d(wring + slot * TMA_WPLANE, wm, x0 - 2, y0 - 1, z0 - 1 + p + wzoff, &wfull[slot]);
+                    mbar_expect_tx(&wfull[slot], WBYTES);
+                    const int zc_ = z0 - 1 + p + wzoff;
+                    if constexpr (TWO_D) {
+#pragma unroll
+                        for (int cpy = 0; cpy < S::WCOPIES; ++cpy)
+                            tma_load3d(wring + slot * TMA_WPLANE + cpy * S::WBX, wm, x0 - 2 + cpy * S::WBX, 0, zc_,
+                                       &wfull[slot]);
+                    } else {
+                        tma_load3d(wring + slot * TMA_WPLANE, wm, x0 - 2, y0 - 1, zc_, &wfull[slot]);
+                    }
                     ++p;
                 } else {
                     const int slot = q % SS;
@@ -144,21 +170,23 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
                     mbar_expect_tx(&sfull[slot], SBYTES);
 #pragma unroll
                     for (int s = 0; s < NSTR; ++s)
-                        tma_load3d(sring + (slot * NSTR + s) * TMA_SPLANE, &maps.s[s], x0, y0, z0 + q,
-                                   &sfull[slot]);
+#pragma unroll
+                        for (int cpy = 0; cpy < S::SCOPIES; ++cpy)
+                            tma_load3d(sring + (slot * NSTR + s) * TMA_SPLANE + cpy * S::SBX, &maps.s[s],
+                                       x0 + cpy * S::SBX, y0, z0 + q, &sfull[slot]);
                     ++q;
                 }
             }
         }
     } else {
         // ------------------------------------------------------ consumers
-        const int wy = warp;
-        const int xl = 2 * lane;
+        const int wy = TWO_D ? 0 : warp;
+        const int xl = (TWO_D ? warp * 64 : 0) + 2 * lane;
         const long long x = x0 + xl, y = y0 + wy;
         const bool ok = (y < g.NY) && (x < g.NX);
         const long long NX = g.NX, sxy = g.NX * g.NY;
-        const int cw = (wy + 1) * TMA_WX + 2 + xl;           // own pair in a w plane
-        const int cs = wy * TMA_TX + xl;                     // own pair in a stream plane
+        const int cw = (TWO_D ? 0 : (wy + 1) * S::WCOLS) + 2 + xl;   // own pair in a w plane
+        const int cs = wy * S::TX + xl;                               // own pair in a stream plane
         mbar_wait(&wfull[0], 0);
         mbar_wait(&wfull[1 % SW], (1 / SW) & 1);
         for (int k = 0; k < ns; ++k) {
@@ -174,26 +202,30 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
                 const double2 qm = *reinterpret_cast<const double2 *>(Wm + cw);
                 const double2 qc = *reinterpret_cast<const double2 *>(Wc + cw);
                 const double2 qp = *reinterpret_cast<const double2 *>(Wp + cw);
-                const double2 ym = *reinterpret_cast<const double2 *>(Wc + cw - TMA_WX);
-                const double2 yp = *reinterpret_cast<const double2 *>(Wc + cw + TMA_WX);
+                double2 ym = make_double2(0.0, 0.0), yp = make_double2(0.0, 0.0);   // 2D: y ghosts
+                if constexpr (!TWO_D) {
+                    ym = *reinterpret_cast<const double2 *>(Wc + cw - S::WCOLS);
+                    yp = *reinterpret_cast<const double2 *>(Wc + cw + S::WCOLS);
+                }
                 const double xm0 = Wc[cw - 1], xp1 = Wc[cw + 2];
                 typename Body::template Regs<2> R;
                 body.load_tma(Sp, cs, R);
-                // 7-point stencil, terms in ascending column order (as csr_matvec)
+                // 7-point stencil on m = xf(w), terms in ascending column order (as csr_matvec)
                 const double zmv[2] = {qm.x, qm.y}, ymv[2] = {ym.x, ym.y}, xmv[2] = {xm0, qc.x};
                 const double cv[2] = {qc.x, qc.y}, xpv[2] = {qc.y, xp1}, ypv[2] = {yp.x, yp.y},
                              zpv[2] = {qp.x, qp.y};
+                auto xf = [&](double r) { return PCIN ? __dmul_rn(r, cin) : r; };
                 double n[2];
 #pragma unroll
                 for (int v = 0; v < 2; ++v) {
                     double a = 0.0;
-                    a = __dadd_rn(a, -zmv[v]);
-                    a = __dadd_rn(a, -ymv[v]);
-                    a = __dadd_rn(a, -xmv[v]);
-                    a = __dadd_rn(a, __dmul_rn(g.diag, cv[v]));
-                    a = __dadd_rn(a, -xpv[v]);
-                    a = __dadd_rn(a, -ypv[v]);
-                    a = __dadd_rn(a, -zpv[v]);
+                    a = __dadd_rn(a, -xf(zmv[v]));
+                    a = __dadd_rn(a, -xf(ymv[v]));
+                    a = __dadd_rn(a, -xf(xmv[v]));
+                    a = __dadd_rn(a, __dmul_rn(g.diag, xf(cv[v])));
+                    a = __dadd_rn(a, -xf(xpv[v]));
+                    a = __dadd_rn(a, -xf(ypv[v]));
+                    a = __dadd_rn(a, -xf(zpv[v]));
                     n[v] = a;
                 }
                 const long long kk = (long long)z * sxy + x + NX * y;

@@ -157,13 +157,17 @@ def device_precond(M, dm, device) -> DevicePrecond:
     return dp
 
 
-def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk_blocks=0) -> KplOp:
+def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk_blocks=0,
+            geometry=None) -> KplOp:
+    """`geometry` overrides the stencil grid view (e.g. a 2D grid's slab view)."""
     op = KplOp()
     op.kind = dm.kind
     op.precond = dp.code if dp is not None else _lib.KPL_PC_IDENTITY
     op.n = dm.n
     if dm.kind == _lib.KPL_OP_STENCIL:
         op.nx, op.ny, op.nz, op.diag = dm.nx, dm.ny, dm.nz, float(dm.diag)
+        if geometry is not None:
+            op.nx, op.ny, op.nz = geometry
     else:
         op.row_ptr = ptr(dm.row_ptr)
         op.col_idx = ptr(dm.col_idx)

@@ -236,7 +236,7 @@ class DistributedStencilSolve:
         if not hasattr(A, "stencil_spec"):
             raise NotImplementedError("multi-GPU row-block CSR (general halo gather) is not built yet")
         self.device = D.require_cuda()
-        NX, NY, NZ, diag = A.stencil_spec()
+        NX, NY, NZ, diag = A.slab_spec() if hasattr(A, "slab_spec") else A.stencil_spec()
         self.A, self.cfg, self.comm = A, cfg, comm
         self.plan = SlabPlan(NX, NY, NZ, comm.size, zc)
         kind = "identity" if M is None else getattr(M, "kind", "identity")

@@ -34,7 +34,14 @@ class _Stencil:
         self._device = None
 
     def stencil_spec(self):
+        """Device geometry (NX, NY, NZ, diag); id = x + NX*(y + NY*z)."""
         return (self.NX, self.NY, self.NZ, float(self.diag_value))
+
+    def slab_spec(self):
+        """Geometry whose last axis is split into z-slabs by the multi-GPU
+        solver: 3D grids as they are; a 2D grid as (nx, 1, ny), so its rows
+        become the slab axis.  Same element order as stencil_spec."""
+        return self.stencil_spec()
 
     @property
     def mu(self):
@@ -62,7 +69,10 @@ class _Stencil:
 
 
 class Stencil2D(_Stencil):
-    """5-point Laplacian on nx-by-ny (the operator of `laplacian_2d(nx, ny)`)."""
+    """5-point Laplacian on nx-by-ny (the operator of `laplacian_2d(nx, ny)`).
+
+    Runs on the device as the grid (nx, 1, ny): the sweep marches over the
+    rows (the z axis of the 3D machinery) with 512-wide row tiles."""
 
     diag_value = 4.0
 

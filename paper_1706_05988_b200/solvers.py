@@ -163,7 +163,7 @@ class SolverState:
 class _Solve:
     """One solve: device vectors, workspace, and the host enqueue loop."""
 
-    def __init__(self, A, M, b, x0, cfg: SolverConfig, *, zc=0, vx=0, chunk_blocks=0):
+    def __init__(self, A, M, b, x0, cfg: SolverConfig, *, zc=0, vx=0, chunk_blocks=0, slab_view=False):
         self.device = dev = D.require_cuda()
         t = D.torch()
         self.cfg = cfg
@@ -175,7 +175,8 @@ class _Solve:
         self.x0 = None
         if x0 is not None:
             self.x0, _ = D.to_device_f64(x0, n, dev, "initial guess")
-        self.op = D.make_op(self.dm, self.dp, zc=zc, vx=vx, chunk_blocks=chunk_blocks)
+        geom = A.slab_spec()[:3] if (slab_view and hasattr(A, "slab_spec")) else None
+        self.op = D.make_op(self.dm, self.dp, zc=zc, vx=vx, chunk_blocks=chunk_blocks, geometry=geom)
         self.kcfg, self._keep = make_kcfg(cfg, A, self.dm, dev)
         ident = self.dp.identity
         f64 = dict(dtype=t.float64, device=dev)

@@ -125,8 +125,9 @@ gpu = pytest.mark.gpu
 
 
 def _one_gpu(A, M, b, cfg, zc):
+    """1-GPU solve in the geometry the slab partition uses (2D grids: (nx, 1, ny))."""
     from paper_1706_05988_b200.solvers import _Solve
-    return _Solve(A, M, b, None, cfg, zc=zc).run()
+    return _Solve(A, M, b, None, cfg, zc=zc, slab_view=True).run()
 
 
 @gpu
