@@ -207,6 +207,9 @@ int kpl_sweep(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, int32_t k
 int kpl_sweep_phase(int32_t kind);
 
 /* ---- multi-GPU hooks (one process per GPU; host drives NCCL) ----------- */
+/* dst[k] = src[idx[k]] for k < n: packs the rows a neighbour needs (the
+   general halo gather of row-block CSR partitions).                        */
+int kpl_gather(int64_t n, const int32_t *idx, const double *src, double *dst, void *stream);
 /* Level-4 fold of the gathered chunk table + the scalar epilogue of sweep
    `kind` (same predicate as the sweep).  Every rank runs it on identical
    data, so every rank holds identical scalars and history.                */

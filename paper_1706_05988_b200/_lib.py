@@ -68,6 +68,7 @@ _SIGS = {
     "kpl_spmv": (_i32, [ctypes.POINTER(KplOp), _p, _p, _p]),
     "kpl_dot": (_i32, [ctypes.POINTER(KplOp), _p, _p, _p, _p, _p]),
     "kpl_axpy": (_i32, [_i64, _d, _p, _p, _p, _p]),
+    "kpl_gather": (_i32, [_i64, _p, _p, _p, _p]),
     "kpl_solver_init": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
                                ctypes.POINTER(KplVecs), _p, _p, _p]),
     "kpl_solver_iterate": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),

@@ -296,6 +296,12 @@ __global__ void head_init_kernel(WsHead *h, double *hist, long long nrows, unsig
     for (long long k = tid; k < ncnt; k += gridDim.x * (long long)blockDim.x) cnt[k] = 0u;
 }
 
+__global__ void gather_kernel(long long n, const int *__restrict__ idx, const double *__restrict__ src,
+                              double *__restrict__ dst) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += gridDim.x * (long long)blockDim.x)
+        dst[k] = __ldg(src + idx[k]);
+}
+
 __global__ void axpy_kernel(long long n, double a, const double *__restrict__ x, const double *__restrict__ y,
                             double *__restrict__ out) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += gridDim.x * (long long)blockDim.x)
@@ -411,6 +417,15 @@ int kpl_axpy(int64_t n, double alpha, const double *x, const double *y, double *
     g_launches.fetch_add(1, std::memory_order_relaxed);
     axpy_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(n, alpha, x, y, out);
     return cuda_check("axpy");
+}
+
+int kpl_gather(int64_t n, const int32_t *idx, const double *src, double *dst, void *stream) {
+    if (n < 0) return fail(KPL_EINVAL, "negative length");
+    if (n == 0) return KPL_OK;
+    const long long blocks = std::min<long long>(cdiv(n, 256), 148LL * 8);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    gather_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
+    return cuda_check("gather");
 }
 
 int kpl_read_status(const void *workspace, kpl_status *out, void *stream) {

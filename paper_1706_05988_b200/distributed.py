@@ -21,9 +21,16 @@ one process on one device (exchanges and gathers become device copies; all
 sweeps are launched sequentially, none waits on another) -- the single-GPU
 stand-in used by the parity tests.
 
-Scope: stencil operators, identity or constant-diagonal Jacobi, every method
-(cg / pcg / pcg_sh / pcg_var_sh / pcg_rr) and track_gaps.  Row-block CSR with
-general halo gathers is not built yet (raises NotImplementedError).
+Row-block CSR.  `RowPlan` cuts the rows into chunk-aligned blocks; every
+rank keeps its rows of the matrix with columns remapped to [local rows |
+ghosts], where the ghosts are the sorted remote columns its rows touch.  Per
+sweep the owners pack the requested rows (kpl_gather) and send them to the
+ghost segments (NCCL send/recv); the Jacobi inverse diagonal of the ghosts is
+static and copied once.
+
+Scope: stencils (identity or constant-diagonal Jacobi) and CSR (identity or
+Jacobi); every method (cg / pcg / pcg_sh / pcg_var_sh / pcg_rr) and
+track_gaps.
 """
 
 from __future__ import annotations
@@ -64,60 +71,43 @@ class SlabPlan:
 
 
 class _RankState:
-    """Device state of one rank (vectors with halo planes, op, workspace)."""
+    """Device state of one rank: vectors (interior + halo/ghost storage), op,
+    kcfg, workspace and its chunk-table views.  Subclasses define the layout."""
 
     VEC_NAMES = ("x", "r", "u", "w0", "w1", "z", "q", "s", "t", "p", "p1")
 
-    def __init__(self, plan: SlabPlan, rank, diag, pc_code, pc_const, cfg: SolverConfig, device, kcfg):
+    def _alloc_vectors(self, cfg, ident, n, extra, device):
+        """Every state vector as one tensor of n + extra values (extra = halo
+        or ghost storage); identity aliases u=r, q=s, p=t as on one GPU."""
         t = D.torch()
-        self.plan, self.rank, self.device = plan, rank, device
-        self.cfg = cfg
-        self.ident = pc_code == _lib.KPL_PC_IDENTITY
-        n, sxy = plan.n_local, plan.sxy
         f64 = dict(dtype=t.float64, device=device)
-        self.full = {}                  # name -> (nzl+2)*sxy tensor incl. halos
-
-        def vec():
-            return t.zeros(n + 2 * sxy, **f64)
-
+        self.full = {}
         names = ["x", "r"]
-        if not self.ident:
+        if not ident:
             names.append("u")
         if cfg.method == "cg":
             names += ["p", "p1", "s"]
         else:
             names += ["w0", "w1", "z", "s", "t"]
-            if not self.ident:
+            if not ident:
                 names += ["q", "p"]
         for nm in names:
-            self.full[nm] = vec()
-        if self.ident:
+            self.full[nm] = t.zeros(n + extra, **f64)
+        if ident:
             self.full["u"] = self.full["r"]
             if cfg.method != "cg":
                 self.full["q"] = self.full["s"]
                 self.full["p"] = self.full["t"]
         self.b = t.zeros(n, **f64)
 
-        op = _lib.KplOp()
-        op.kind = _lib.KPL_OP_STENCIL
-        op.precond = pc_code
-        op.n = n
-        op.nx, op.ny, op.nz, op.diag = plan.NX, plan.NY, plan.nzl, float(diag)
-        op.zc = plan.zc
-        op.zhalo = 1
-        op.pc_const = pc_const
-        op.chunk_offset = rank * plan.chunks_local
-        op.chunks_global = plan.chunks_global
-        self.op = op
-
-        self.kcfg = kcfg
-
+    def _finish(self, op, cfg, kcfg, device, chunks_local):
+        t = D.torch()
+        self.op, self.kcfg, self.cfg = op, kcfg, cfg
         v = _lib.KplVecs()
         for nm in self.VEC_NAMES:
             setattr(v, nm, D.ptr(self.interior(nm)) if nm in self.full else None)
         v.b = D.ptr(self.b)
         self.vecs = v
-
         lib = _lib.load()
         nbytes = lib.kpl_workspace_bytes(op, cfg.max_iters)
         _lib.check(nbytes if nbytes < 0 else 0, "workspace size")
@@ -126,22 +116,14 @@ class _RankState:
         _lib.check(lib.kpl_chunk_table(op, D.ptr(self.ws), loc, glob, lbytes), "chunk table")
         base = self.ws.data_ptr()
         g0 = glob.value - base
-        l0 = loc.value - base
-        nb = 8 * 4 * plan.chunks_global
+        nb = 8 * 4 * int(op.chunks_global)
         self.table = self.ws[g0:g0 + nb].view(t.float64)
-        self.table_local = self.ws[l0:l0 + lbytes.value].view(t.float64)
+        self.chunk_offset = int(op.chunk_offset)
+        self.chunks_local = chunks_local
+        self.table_local = self.table[4 * self.chunk_offset:4 * (self.chunk_offset + chunks_local)]
         self.hist_off = lib.kpl_history_offset(op)
         self.reps_off = lib.kpl_replacements_offset(op, cfg.max_iters)
         self.status = _lib.KplStatus()
-
-    def interior(self, name):
-        sxy = self.plan.sxy
-        return self.full[name][sxy:sxy + self.plan.n_local]
-
-    def planes(self, name):
-        """(lower halo, first plane, last plane, upper halo) views."""
-        f, sxy, n = self.full[name], self.plan.sxy, self.plan.n_local
-        return f[:sxy], f[sxy:2 * sxy], f[n:n + sxy], f[n + sxy:]
 
     # -- device calls
     def prepare(self):
@@ -167,8 +149,145 @@ class _RankState:
         return raw.view(t.float64).reshape(rows, HC).cpu().numpy()
 
 
+class _SlabState(_RankState):
+    """z-slab of a stencil grid: vectors carry one halo plane on each side."""
+
+    def __init__(self, plan: SlabPlan, rank, diag, pc_code, pc_const, cfg, device, kcfg):
+        self.plan, self.rank, self.device = plan, rank, device
+        self.ident = pc_code == _lib.KPL_PC_IDENTITY
+        n, sxy = plan.n_local, plan.sxy
+        self._alloc_vectors(cfg, self.ident, n, 2 * sxy, device)
+        op = _lib.KplOp()
+        op.kind = _lib.KPL_OP_STENCIL
+        op.precond = pc_code
+        op.n = n
+        op.nx, op.ny, op.nz, op.diag = plan.NX, plan.NY, plan.nzl, float(diag)
+        op.zc = plan.zc
+        op.zhalo = 1
+        op.pc_const = pc_const
+        op.chunk_offset = rank * plan.chunks_local
+        op.chunks_global = plan.chunks_global
+        self._finish(op, cfg, kcfg, device, plan.chunks_local)
+
+    def interior(self, name):
+        sxy = self.plan.sxy
+        return self.full[name][sxy:sxy + self.plan.n_local]
+
+    def planes(self, name):
+        """(lower halo, first plane, last plane, upper halo) views."""
+        f, sxy, n = self.full[name], self.plan.sxy, self.plan.n_local
+        return f[:sxy], f[sxy:2 * sxy], f[n:n + sxy], f[n + sxy:]
+
+
+class RowPlan:
+    """Row-block partition of a CSR matrix over P ranks with general halo
+    (ghost) gathers.  Block boundaries are multiples of one reduction chunk
+    (chunk_blocks x 256 rows), so every rank's chunk partials are the ones a
+    single GPU computes for those rows and the gathered fold is bit-identical.
+
+    Every rank holds the host matrix, so every rank derives every rank's ghost
+    and send lists locally -- no setup communication."""
+
+    def __init__(self, A, P, chunk_blocks=8):
+        n = int(A.n)
+        self.n, self.P = n, P
+        self.chunk_rows = 256 * chunk_blocks
+        self.chunk_blocks = chunk_blocks
+        al = self.chunk_rows
+        starts = [min(n, ((r * n) // P) // al * al) for r in range(P)] + [n]
+        if any(starts[r + 1] <= starts[r] for r in range(P)):
+            raise ValueError(f"{n} rows are too few for {P} ranks of {al}-row chunks")
+        self.starts = starts
+        self.chunks_global = -(-n // al)
+        rp = np.asarray(A.row_ptr, dtype=np.int64)
+        ci = np.asarray(A.col_idx, dtype=np.int64)
+        self.ranks = []
+        for r in range(P):
+            r0, r1 = starts[r], starts[r + 1]
+            k0, k1 = int(rp[r0]), int(rp[r1])
+            cols = ci[k0:k1]
+            remote = (cols < r0) | (cols >= r1)
+            ghosts = np.unique(cols[remote])
+            owner = np.searchsorted(np.asarray(starts), ghosts, side="right") - 1
+            local = np.where(remote, 0, cols - r0)
+            gpos = np.searchsorted(ghosts, cols[remote])
+            local[remote] = (r1 - r0) + gpos
+            recv = {}
+            for q in np.unique(owner):
+                sel = np.nonzero(owner == q)[0]
+                recv[int(q)] = (int(sel[0]), len(sel), ghosts[sel] - starts[q])   # offset, count, q-local rows
+            self.ranks.append(dict(r0=r0, r1=r1, k0=k0, k1=k1, ghosts=ghosts, recv=recv,
+                                   row_ptr=(rp[r0:r1 + 1] - k0).astype(np.int32),
+                                   col_idx=local.astype(np.int32)))
+        # send lists: rank q sends to r the q-local rows listed in r's recv[q]
+        for r in range(P):
+            self.ranks[r]["send"] = {}
+        for r in range(P):
+            for q, (off, cnt, qrows) in self.ranks[r]["recv"].items():
+                self.ranks[q]["send"][r] = qrows
+
+    def local_slice(self, rank):
+        return slice(self.starts[rank], self.starts[rank + 1])
+
+    def chunk_offset(self, rank):
+        return self.starts[rank] // self.chunk_rows
+
+    def chunks_local(self, rank):
+        return -(-(self.starts[rank + 1] - self.starts[rank]) // self.chunk_rows)
+
+
+class _RowState(_RankState):
+    """Row block of a CSR matrix: vectors = [local rows | ghost values]."""
+
+    def __init__(self, plan: RowPlan, rank, A, M, pc_code, cfg, device, kcfg):
+        t = D.torch()
+        self.plan, self.rank, self.device = plan, rank, device
+        self.ident = pc_code == _lib.KPL_PC_IDENTITY
+        info = plan.ranks[rank]
+        n = info["r1"] - info["r0"]
+        self.n_local, self.n_ghost = n, len(info["ghosts"])
+        self._alloc_vectors(cfg, self.ident, n, self.n_ghost, device)
+        up = lambda a, dt: t.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
+        self.row_ptr = up(info["row_ptr"], np.int32)
+        self.col_idx = up(info["col_idx"], np.int32)
+        self.values = up(np.asarray(A.values)[info["k0"]:info["k1"]], np.float64)
+        op = _lib.KplOp()
+        op.kind = _lib.KPL_OP_CSR
+        op.precond = pc_code
+        op.n = n
+        op.row_ptr, op.col_idx, op.values = D.ptr(self.row_ptr), D.ptr(self.col_idx), D.ptr(self.values)
+        op.nnz = info["k1"] - info["k0"]
+        op.chunk_blocks = plan.chunk_blocks
+        self.dinv = None
+        if pc_code == _lib.KPL_PC_JACOBI_VEC:
+            inv = np.asarray(M.inv_diag, dtype=np.float64)
+            # inverse diagonal of the local rows followed by the ghosts' (static, no exchange)
+            self.dinv = up(np.concatenate([inv[info["r0"]:info["r1"]], inv[info["ghosts"]]]), np.float64)
+            op.inv_diag = D.ptr(self.dinv)
+        op.chunk_offset = plan.chunk_offset(rank)
+        op.chunks_global = plan.chunks_global
+        self.recv = {q: (off, cnt) for q, (off, cnt, _) in info["recv"].items()}
+        self.send_idx = {q: up(rows, np.int32) for q, rows in info["send"].items()}
+        self.send_buf = {q: t.empty(len(rows), dtype=t.float64, device=device)
+                         for q, rows in info["send"].items()}
+        self._finish(op, cfg, kcfg, device, plan.chunks_local(rank))
+
+    def interior(self, name):
+        return self.full[name][:self.n_local]
+
+    def ghost(self, name, q):
+        off, cnt = self.recv[q]
+        return self.full[name][self.n_local + off:self.n_local + off + cnt]
+
+
+def _gather(idx, src, dst):
+    """dst[k] = src[idx[k]] on the device (kpl_gather)."""
+    _lib.check(_lib.load().kpl_gather(idx.numel(), D.ptr(idx), D.ptr(src), D.ptr(dst),
+                                      D.stream_handle()), "gather")
+
+
 class LocalComm:
-    """P ranks as P slab states in one process on one device."""
+    """P ranks as P states in one process on one device (parity tests)."""
 
     def __init__(self, P):
         self.size = P
@@ -180,19 +299,23 @@ class LocalComm:
     def exchange(self, states, name):
         for s in states:
             r = s.rank
-            lo, first, last, hi = s.planes(name)
-            if r > 0:
-                lo.copy_(states[r - 1].planes(name)[2])
-            if r < self.size - 1:
-                hi.copy_(states[r + 1].planes(name)[1])
+            if isinstance(s, _SlabState):
+                lo, first, last, hi = s.planes(name)
+                if r > 0:
+                    lo.copy_(states[r - 1].planes(name)[2])
+                if r < self.size - 1:
+                    hi.copy_(states[r + 1].planes(name)[1])
+            else:
+                for q in s.recv:
+                    src = states[q]
+                    _gather(src.send_idx[r], src.interior(name), s.ghost(name, q))
 
     def allgather(self, states):
         for dst in states:
             for src in states:
                 if src is not dst:
-                    n = src.table_local.numel()
-                    off = src.rank * n
-                    dst.table[off:off + n].copy_(src.table_local)
+                    o, n = 4 * src.chunk_offset, 4 * src.chunks_local
+                    dst.table[o:o + n].copy_(src.table_local)
 
 
 class TorchComm:
@@ -204,6 +327,7 @@ class TorchComm:
         self.group = group
         self.size = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self._counts = None
 
     def local_ranks(self):
         return [self.rank]
@@ -211,35 +335,70 @@ class TorchComm:
     def exchange(self, states, name):
         dist = self.dist
         (s,) = states
-        lo, first, last, hi = s.planes(name)
         ops = []
-        if s.rank > 0:
-            ops.append(dist.P2POp(dist.isend, first.contiguous(), s.rank - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, lo, s.rank - 1, self.group))
-        if s.rank < self.size - 1:
-            ops.append(dist.P2POp(dist.isend, last.contiguous(), s.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, hi, s.rank + 1, self.group))
+        if isinstance(s, _SlabState):
+            lo, first, last, hi = s.planes(name)
+            if s.rank > 0:
+                ops.append(dist.P2POp(dist.isend, first.contiguous(), s.rank - 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, lo, s.rank - 1, self.group))
+            if s.rank < self.size - 1:
+                ops.append(dist.P2POp(dist.isend, last.contiguous(), s.rank + 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, hi, s.rank + 1, self.group))
+        else:
+            for q, idx in s.send_idx.items():          # pack the rows each peer needs
+                _gather(idx, s.interior(name), s.send_buf[q])
+                ops.append(dist.P2POp(dist.isend, s.send_buf[q], q, self.group))
+            for q in s.recv:
+                ops.append(dist.P2POp(dist.irecv, s.ghost(name, q), q, self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
 
     def allgather(self, states):
         (s,) = states
-        # in-place all-gather: this rank's slice already sits at offset rank*count
-        self.dist.all_gather_into_tensor(s.table, s.table_local.clone(), group=self.group)
+        t = D.torch()
+        if self._counts is None:
+            c = t.tensor([s.chunks_local], dtype=t.int64, device=s.table.device)
+            allc = [t.zeros_like(c) for _ in range(self.size)]
+            self.dist.all_gather(allc, c, group=self.group)
+            self._counts = [int(v.item()) for v in allc]
+        counts = self._counts
+        if all(c == counts[0] for c in counts):
+            # in-place all-gather: this rank's slice sits at offset rank*count
+            self.dist.all_gather_into_tensor(s.table, s.table_local.clone(), group=self.group)
+            return
+        # uneven row blocks: gather padded slices, then compact in rank order
+        mx = max(counts)
+        buf = t.zeros(4 * mx * self.size, dtype=t.float64, device=s.table.device)
+        mine = t.zeros(4 * mx, dtype=t.float64, device=s.table.device)
+        mine[:s.table_local.numel()].copy_(s.table_local)
+        self.dist.all_gather_into_tensor(buf, mine, group=self.group)
+        off = 0
+        for q, cq in enumerate(counts):
+            s.table[4 * off:4 * (off + cq)].copy_(buf[4 * mx * q:4 * mx * q + 4 * cq])
+            off += cq
 
 
-class DistributedStencilSolve:
-    """Drive one z-slab-partitioned solve; `comm` decides which ranks are local."""
+class DistributedSolve:
+    """Drive one partitioned solve (stencil z-slabs or CSR row blocks);
+    `comm` decides which ranks are local."""
 
-    def __init__(self, A, M, cfg: SolverConfig, comm, zc=0):
-        if not hasattr(A, "stencil_spec"):
-            raise NotImplementedError("multi-GPU row-block CSR (general halo gather) is not built yet")
+    def __init__(self, A, M, cfg: SolverConfig, comm, zc=0, chunk_blocks=8):
         self.device = D.require_cuda()
-        NX, NY, NZ, diag = A.slab_spec() if hasattr(A, "slab_spec") else A.stencil_spec()
         self.A, self.cfg, self.comm = A, cfg, comm
-        self.plan = SlabPlan(NX, NY, NZ, comm.size, zc)
         kind = "identity" if M is None else getattr(M, "kind", "identity")
+        self.limit = cfg.max_iters + (1 if cfg.method == "cg" else 0)
+        if not hasattr(A, "stencil_spec"):
+            if kind not in ("identity", "jacobi"):
+                raise NotImplementedError(f"preconditioner {kind!r} not on the device path")
+            pc = _lib.KPL_PC_IDENTITY if kind == "identity" else _lib.KPL_PC_JACOBI_VEC
+            self.plan = RowPlan(A, comm.size, chunk_blocks)
+            self.kcfg, self._keep = make_kcfg(cfg, A, self, self.device)
+            self.states = [_RowState(self.plan, r, A, M, pc, cfg, self.device, self.kcfg)
+                           for r in comm.local_ranks()]
+            return
+        NX, NY, NZ, diag = A.slab_spec() if hasattr(A, "slab_spec") else A.stencil_spec()
+        self.plan = SlabPlan(NX, NY, NZ, comm.size, zc)
         if kind == "identity":
             pc, c = _lib.KPL_PC_IDENTITY, 0.0
         elif kind == "jacobi":
@@ -253,9 +412,8 @@ class DistributedStencilSolve:
         else:
             raise NotImplementedError(f"preconditioner {kind!r} not on the device path")
         self.kcfg, self._keep = make_kcfg(cfg, A, self, self.device)
-        self.states = [_RankState(self.plan, r, diag, pc, c, cfg, self.device, self.kcfg)
+        self.states = [_SlabState(self.plan, r, diag, pc, c, cfg, self.device, self.kcfg)
                        for r in comm.local_ranks()]
-        self.limit = cfg.max_iters + (1 if cfg.method == "cg" else 0)
 
     # -- collective building blocks
     def _all(self, fn):
@@ -356,15 +514,20 @@ class DistributedStencilSolve:
         return SolveResult(xs, bool(st.converged), rows - 1, history, reps)
 
 
-def solve_distributed(A, M, b_local, x0_local, cfg: SolverConfig, comm=None, zc=0):
-    """z-slab solve on the ranks of `comm` (default: the torch.distributed world).
+DistributedStencilSolve = DistributedSolve       # earlier name
 
-    `b_local` / `x0_local`: this rank's slab (natural order, n/P values), or,
-    with a LocalComm, a list with one slab per rank.  Returns a SolveResult
-    whose `x` is the list of local slabs and whose history is global."""
+
+def solve_distributed(A, M, b_local, x0_local, cfg: SolverConfig, comm=None, zc=0, chunk_blocks=8):
+    """Partitioned solve on the ranks of `comm` (default: the torch.distributed
+    world): stencils by z-slabs (`SlabPlan`), CSR matrices by row blocks with
+    general ghost gathers (`RowPlan`).
+
+    `b_local` / `x0_local`: this rank's rows (plan.local_slice(rank)), or, with
+    a LocalComm, a list with one block per rank.  Returns a SolveResult whose
+    `x` is the list of local blocks and whose history is global."""
     if comm is None:
         comm = TorchComm()
-    S = DistributedStencilSolve(A, M, cfg, comm, zc=zc)
+    S = DistributedSolve(A, M, cfg, comm, zc=zc, chunk_blocks=chunk_blocks)
     if not isinstance(comm, LocalComm):
         b_local = [b_local]
         x0_local = None if x0_local is None else [x0_local]

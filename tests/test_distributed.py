@@ -18,7 +18,8 @@ import pytest
 import torch
 
 from oracle import gpu_order
-from paper_1706_05988_b200.distributed import SlabPlan, TorchComm
+from paper_1706_05988_b200 import distributed as dmod
+from paper_1706_05988_b200.distributed import RowPlan, SlabPlan, TorchComm
 
 
 def free_port():
@@ -58,11 +59,12 @@ def test_reduction_partition_invariant(P, dims, vx, wx, wy):
     assert gpu_order.reduce_items(chunks) == whole
 
 
-class _FakeState:
-    """Stand-in rank state with CPU tensors (plumbing test only)."""
+class _FakeState(dmod._SlabState):
+    """Stand-in slab state with CPU tensors (plumbing test only)."""
 
     def __init__(self, rank, P, sxy, nzl, chunks):
         self.rank = rank
+        self.chunk_offset, self.chunks_local = rank * chunks, chunks
         self.sxy, self.nzl = sxy, nzl
         self.full = {"w0": torch.zeros((nzl + 2) * sxy, dtype=torch.float64)}
         self.full["w0"][sxy:(nzl + 1) * sxy] = torch.arange(nzl * sxy, dtype=torch.float64) + 1000 * rank
@@ -197,3 +199,123 @@ def test_local_ranks_gaps_bitwise(method, extra):
         assert (a.gap_f, a.gap_g, a.gap_h, a.gap_j, a.rnorm_true) == \
                (c.gap_f, c.gap_g, c.gap_h, c.gap_j, c.rnorm_true)
         assert (a.alpha, a.beta) == (c.alpha, c.beta)
+
+
+def test_row_plan_ghost_mapping_reproduces_global_spmv():
+    """Local rows with remapped columns [local | ghosts] and the plan's
+    send/recv lists reproduce the global csr_matvec bit for bit."""
+    from oracle import kpl_oracle as O
+    from paper_1706_05988_b200 import problems
+    A = problems.banded_spd(20000, seed=0, band=3000)
+    v = np.random.default_rng(3).normal(size=A.n)
+    want = O.spmv(O.CSR(A.n, A.row_ptr, A.col_idx, A.values), v)
+    for P in (2, 3, 5):
+        plan = RowPlan(A, P, chunk_blocks=2)
+        for r in range(P):
+            info = plan.ranks[r]
+            ext = np.concatenate([v[plan.local_slice(r)], v[info["ghosts"]]])
+            # the ghost segment from each owner equals that owner's packed send list
+            for q, (off, cnt, qrows) in info["recv"].items():
+                sent = v[plan.local_slice(q)][plan.ranks[q]["send"][r]]
+                assert sent.tobytes() == ext[len(ext) - len(info["ghosts"]) + off:][:cnt].tobytes()
+            n_loc = info["r1"] - info["r0"]
+            Aloc = O.CSR(n_loc, info["row_ptr"], info["col_idx"],
+                         np.asarray(A.values)[info["k0"]:info["k1"]])
+            got = O.spmv(Aloc, ext) if n_loc else np.zeros(0)
+            assert got.tobytes() == want[plan.local_slice(r)].tobytes()
+        assert plan.starts[0] == 0 and all(s % plan.chunk_rows == 0 for s in plan.starts[:-1])
+
+
+@gpu
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("method,extra", [("pcg_sh", {"shift": 0.4124626382901352}), ("cg", {}),
+                                          ("pcg_rr", {})])
+def test_local_ranks_csr_bitwise(P, method, extra):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200 import problems
+    from paper_1706_05988_b200.distributed import LocalComm, solve_distributed
+    A = problems.banded_spd(20000, seed=0, band=2000)
+    M = K.make_jacobi(A)
+    b = K.spmv(A, np.random.default_rng(1).standard_normal(A.n))
+    cfg = K.SolverConfig(method=method, max_iters=300, rtol=1e-10, **extra)
+    ref = K.solve(A, M, b, None, cfg)
+    plan = RowPlan(A, P)
+    res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
+                            comm=LocalComm(P))
+    x = np.concatenate([xi.cpu().numpy() for xi in res.x])
+    assert res.iterations == ref.iterations and res.converged == ref.converged
+    for a, c in zip(res.history, ref.history):
+        assert (a.alpha, a.beta, a.gamma, a.delta, a.rnorm_recursive, a.rnorm_true) == \
+               (c.alpha, c.beta, c.gamma, c.delta, c.rnorm_recursive, c.rnorm_true)
+    assert x.tobytes() == ref.x.tobytes()
+    assert res.replacements == ref.replacements
+
+
+@gpu
+def test_local_ranks_csr_varcoef_identity_bitwise():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200 import problems
+    from paper_1706_05988_b200.distributed import LocalComm, solve_distributed
+    A = problems.varcoef_3d(24, seed=0)          # 13824 rows
+    b = np.random.default_rng(1).standard_normal(A.n)
+    cfg = K.SolverConfig(method="pcg_sh", shift=0.3, max_iters=150, rtol=0.0, track_gaps=True)
+    ref = K.solve(A, None, b, None, cfg)
+    plan = RowPlan(A, 2)
+    res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(2)], None, cfg,
+                            comm=LocalComm(2))
+    for a, c in zip(res.history, ref.history):
+        assert (a.alpha, a.gap_f, a.gap_g, a.gap_h, a.gap_j) == (c.alpha, c.gap_f, c.gap_g, c.gap_h, c.gap_j)
+
+
+class _FakeRowState(dmod._RowState):
+    """Row-block state with CPU tensors built from a real RowPlan (plumbing only)."""
+
+    def __init__(self, plan, rank, v):
+        info = plan.ranks[rank]
+        self.plan, self.rank = plan, rank
+        self.n_local, self.n_ghost = info["r1"] - info["r0"], len(info["ghosts"])
+        self.full = {"w0": torch.zeros(self.n_local + self.n_ghost, dtype=torch.float64)}
+        self.full["w0"][:self.n_local] = torch.as_tensor(v[plan.local_slice(rank)])
+        self.recv = {q: (off, cnt) for q, (off, cnt, _) in info["recv"].items()}
+        self.send_idx = {q: torch.as_tensor(rows.astype(np.int64)) for q, rows in info["send"].items()}
+        self.send_buf = {q: torch.zeros(len(rows), dtype=torch.float64) for q, rows in info["send"].items()}
+
+
+def _gloo_row_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1706_05988_b200 import problems
+        dmod._gather = lambda idx, src, dst: dst.copy_(src[idx])      # CPU stand-in for kpl_gather
+        A = problems.banded_spd(12000, seed=0, band=1500)
+        plan = RowPlan(A, world, chunk_blocks=2)
+        v = np.arange(A.n, dtype=np.float64) * 0.5
+        s = _FakeRowState(plan, rank, v)
+        TorchComm().exchange([s], "w0")
+        ghosts = s.full["w0"][s.n_local:].numpy()
+        q.put((rank, bool(np.array_equal(ghosts, v[plan.ranks[rank]["ghosts"]])), len(ghosts)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_row_ghost_exchange():
+    """TorchComm's general ghost gather (pack -> send/recv -> ghost segments), world_size 2."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_gloo_row_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, ng in res:
+        assert ok and ng > 0, (rank, ng)
