@@ -191,12 +191,15 @@ struct BodyInitW {
     double *w;
     double sigma;
     int ident;
-    template <int V> struct Regs { double r[V], u[V]; };
+    const double *dinv;    // with mout: m = w * inv_diag for the CSR SpMV
+    double *mout;
+    template <int V> struct Regs { double r[V], u[V], d[V]; };
     static constexpr int kTmaStreams = 1;                 // r (identity preconditioner: u == r)
     __device__ void setup(const Ws &) {}
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
         ld_cs<V>(r, k, R.r);
         if (!ident) ld_cs<V>(u, k, R.u);
+        if (mout) ld_cs<V>(dinv, k, R.d);
     }
     __device__ void load_tma(const double *S, int cs, Regs<2> &R) const { sm2(S, 0, cs, R.r); }
     template <int V>
@@ -213,6 +216,12 @@ struct BodyInitW {
             acc[2][v] = __dadd_rn(acc[2][v], __dmul_rn(R.r[v], R.r[v]));
         }
         st_cs<V>(w, k, ww);
+        if (mout) {
+            double mm[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) mm[v] = __dmul_rn(ww[v], R.d[v]);
+            st_cs<V>(mout, k, mm);
+        }
     }
 };
 
@@ -240,6 +249,7 @@ struct BodyPcgIter {
     double *wout;
     const double *schedule;
     double dsig;
+    double *mout;          // CSR + vector Jacobi: also store m = w * inv_diag (next SpMV input)
     template <int V> struct Regs { double x[V], r[V], z[V], s[V], t[V], u[V], q[V], p[V], d[V]; };
     // x, r, z, s, t (+ u, q, p with a constant-diagonal Jacobi)
     static constexpr int kTmaStreams = PC == KPL_PC_IDENTITY ? 5 : 8;
@@ -326,6 +336,14 @@ struct BodyPcgIter {
             st_cs<V>(u, k, uo);
             st_cs<V>(q, k, qo);
             st_cs<V>(p, k, po);
+        }
+        if constexpr (PC == KPL_PC_JACOBI_VEC) {
+            if (mout) {
+                double mo[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) mo[v] = __dmul_rn(wo[v], R.d[v]);   // precond.py:89
+                st_cs<V>(mout, k, mo);
+            }
         }
     }
 };
@@ -453,15 +471,27 @@ struct BodyRepl {
     const double *dinv;
     double c;
     double *wout;
+    double *mout;          // mode 0, CSR + vector Jacobi: m = w * inv_diag
     template <int V> struct Regs { double d[V]; };
     __device__ void setup(const Ws &ws) { wout = const_cast<double *>(pick(ws.head, SEL_ITER1, w0, w1)); }
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
-        if constexpr (PC == KPL_PC_JACOBI_VEC) { if (mode == 1) ld_cs<V>(dinv, k, R.d); }
+        if constexpr (PC == KPL_PC_JACOBI_VEC) { if (mode == 1 || mout) ld_cs<V>(dinv, k, R.d); }
     }
     template <int V>
     __device__ void compute(long long k, const Regs<V> &R, const double (&n)[V], const double (&)[V],
                             double (&)[1][V]) const {
-        if (mode == 0) { st_cs<V>(wout, k, n); return; }
+        if (mode == 0) {
+            st_cs<V>(wout, k, n);
+            if constexpr (PC == KPL_PC_JACOBI_VEC) {
+                if (mout) {
+                    double mm[V];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) mm[v] = __dmul_rn(n[v], R.d[v]);
+                    st_cs<V>(mout, k, mm);
+                }
+            }
+            return;
+        }
         st_cs<V>(s, k, n);
         if constexpr (PC != KPL_PC_IDENTITY) {
             double qq[V];

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <string>
 #include <atomic>
+#include <type_traits>
 #include <algorithm>
 
 #include <cudaTypedefs.h>
@@ -84,7 +85,13 @@ int make_layout(const kpl_op *op, Layout &L) {
     return fail(KPL_EINVAL, "unknown operator kind");
 }
 
-struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, total; };
+struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, mbuf, total; };
+
+// CSR with a vector Jacobi on one GPU keeps m = w * inv_diag next to w, so the
+// SpMV gathers one vector per nonzero instead of two (w and inv_diag).
+bool use_mbuf(const kpl_op *op) {
+    return op->kind == KPL_OP_CSR && op->row_ptr && op->precond == KPL_PC_JACOBI_VEC && op->chunks_global <= 0;
+}
 
 Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     Offsets o;
@@ -95,7 +102,8 @@ Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     o.hist = o.cnt + align256(4LL * L.nch);
     o.reps = o.hist + align256(8LL * HC * (max_iters + 1));
     o.nbuf = o.reps + align256(8LL * (max_iters + 1));
-    o.total = o.nbuf + (op->kind == KPL_OP_CSR && op->row_ptr ? align256(8LL * op->n) : 0);
+    o.mbuf = o.nbuf + (op->kind == KPL_OP_CSR && op->row_ptr ? align256(8LL * op->n) : 0);
+    o.total = o.mbuf + (use_mbuf(op) ? align256(8LL * op->n) : 0);
     return o;
 }
 
@@ -110,6 +118,7 @@ Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspa
     ws.hist = reinterpret_cast<double *>(base + o.hist);
     ws.reps = reinterpret_cast<long long *>(base + o.reps);
     ws.nbuf = reinterpret_cast<double *>(base + o.nbuf);
+    ws.mbuf = use_mbuf(op) ? reinterpret_cast<double *>(base + o.mbuf) : nullptr;
     ws.chunk_offset = op->chunks_global > 0 ? op->chunk_offset : 0;
     ws.chunks_global = op->chunks_global > 0 ? op->chunks_global : L.nch;
     ws.inline_final = op->chunks_global > 0 ? 0 : 1;
@@ -130,9 +139,13 @@ Cfg make_cfg(const kpl_cfg *c) {
 }
 
 // ------------------------------------------------------------ dispatch
-template <class In, class Body>
+struct NoSpmvIn {};
+
+// `spin`: input of the CSR SpMV when it differs from the body's stencil input
+// (m = w * inv_diag materialised in the workspace); NoSpmvIn = use `in`.
+template <class In, class Body, class SpIn = NoSpmvIn>
 int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, const Cfg &cfg,
-           int phase, int pred, long long row, cudaStream_t st) {
+           int phase, int pred, long long row, cudaStream_t st, SpIn spin = SpIn()) {
     if (L.items <= 0) return KPL_OK;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (op->kind == KPL_OP_STENCIL) {
@@ -146,7 +159,10 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
         CGeo g{op->n, op->row_ptr, op->col_idx, op->values};
         if constexpr (Body::kStencil) {
             g_launches.fetch_add(1, std::memory_order_relaxed);
-            csr_spmv_kernel<In><<<(unsigned)L.items, NT, 0, st>>>(g, in, ws.nbuf, ws, pred, row);
+            if constexpr (std::is_same<SpIn, NoSpmvIn>::value)
+                csr_spmv_kernel<In><<<(unsigned)L.items, NT, 0, st>>>(g, in, ws.nbuf, ws, pred, row);
+            else
+                csr_spmv_kernel<SpIn><<<(unsigned)L.items, NT, 0, st>>>(g, spin, ws.nbuf, ws, pred, row);
         }
         csr_chunk_sweep<In, Body><<<(unsigned)L.nch, NT, 0, st>>>(g, L, in, body, ws.nbuf, ws, cfg, phase, pred,
                                                                  row);
@@ -528,6 +544,7 @@ int do_sweep(const Ctx &c, int kind, long long row) {
     case KPL_SW_INIT_W: {                // w = axpy(-sigma, r, A u) + first reductions (:376, :388-390)
         BodyInitW body;
         body.r = v->r; body.u = u; body.w = v->w0; body.sigma = c.sigma; body.ident = c.ident;
+        body.dinv = op->inv_diag; body.mout = c.ws.mbuf;
         if (tma) {
             const double *streams[1] = {v->r};
             return launch_tma(op, L, u, u, 0, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
@@ -555,13 +572,19 @@ int do_sweep(const Ctx &c, int kind, long long row) {
                 body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = 0.0; body.dsig = 0.0;
                 body.schedule = c.cfg.schedule; body.want_xi = 0;
                 body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
+                body.mout = c.ws.mbuf;
+                if constexpr (PC == KPL_PC_JACOBI_VEC) {
+                    if (c.ws.mbuf)
+                        return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred,
+                                      row, c.st, in_vec<KPL_PC_IDENTITY>(op, c.ws.mbuf, c.ws.mbuf, SEL_FIXED));
+                }
                 return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred, row,
                               c.st);
             });
         return with_pc(op, [&](auto pc) -> int {
             constexpr int PC = decltype(pc)::value;
             BodyPcgIter<PC> body;
-            body.schedule = nullptr; body.dsig = 0.0;
+            body.schedule = nullptr; body.dsig = 0.0; body.mout = c.ws.mbuf;
             body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
             body.s = v->s; body.t = v->t; body.p = v->p; body.w0 = v->w0; body.w1 = v->w1;
             body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = c.sigma;
@@ -578,6 +601,11 @@ int do_sweep(const Ctx &c, int kind, long long row) {
                     return launch_tma<BodyPcgIter<PC>, 1>(op, L, v->w0, v->w1, 1, streams, body, c.ws, c.cfg, phase,
                                                           pred, row, c.st);
                 }
+            }
+            if constexpr (PC == KPL_PC_JACOBI_VEC) {
+                if (c.ws.mbuf)      // SpMV on the materialised m (one gather per nonzero)
+                    return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred,
+                                  row, c.st, in_vec<KPL_PC_IDENTITY>(op, c.ws.mbuf, c.ws.mbuf, SEL_FIXED));
             }
             return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred, row,
                           c.st);
@@ -604,7 +632,7 @@ int do_sweep(const Ctx &c, int kind, long long row) {
             BodyRepl<PC> rw;
             rw.mode = kind == KPL_SW_RR_W ? 0 : 1;
             rw.w0 = v->w0; rw.w1 = v->w1; rw.s = v->s; rw.q = v->q; rw.dinv = op->inv_diag;
-            rw.c = op->pc_const; rw.wout = v->w1;
+            rw.c = op->pc_const; rw.wout = v->w1; rw.mout = kind == KPL_SW_RR_W ? c.ws.mbuf : nullptr;
             const double *in = kind == KPL_SW_RR_W ? u : (c.ident ? v->t : v->p);
             return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, in, in, SEL_FIXED), rw, c.ws, c.cfg, phase, pred,
                           row, c.st);

@@ -75,6 +75,7 @@ struct Ws {                   // device view of the caller's workspace
     double *hist;             // [max_iters+1][HC]
     long long *reps;          // [max_iters+1]
     double *nbuf;             // CSR: n = A m of the current sweep (split SpMV / update)
+    double *mbuf;             // CSR + vector Jacobi (1 GPU): m = w * inv_diag, written with w
     long long chunk_offset;   // first global chunk of this rank
     long long chunks_global;
     int inline_final;         // 1: last CTA finalises (single GPU)
