@@ -148,24 +148,29 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
            int phase, int pred, long long row, cudaStream_t st, SpIn spin = SpIn()) {
     if (L.items <= 0) return KPL_OK;
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    // the replacement sweeps are predicated on a rare device trigger: a small
+    // grid striding over the items keeps their idle cost at a few CTAs
+    const long long cap = pred == PRED_FIRE ? 2LL * kSMs : (1LL << 31) - 1;
     if (op->kind == KPL_OP_STENCIL) {
         SGeo g{op->nx, op->ny, op->nz, op->diag, op->halo_lo, op->halo_hi, op->zhalo};
+        const unsigned grid = (unsigned)std::min(L.items, cap);
         if (L.vx == 2)
-            stencil_sweep<2, In, Body><<<(unsigned)L.items, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
+            stencil_sweep<2, In, Body><<<grid, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
         else
-            stencil_sweep<1, In, Body><<<(unsigned)L.items, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
+            stencil_sweep<1, In, Body><<<grid, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
     } else {
         // split CSR: high-occupancy SpMV into the workspace, then the chunk sweep
         CGeo g{op->n, op->row_ptr, op->col_idx, op->values};
         if constexpr (Body::kStencil) {
             g_launches.fetch_add(1, std::memory_order_relaxed);
+            const unsigned sgrid = (unsigned)std::min(L.items, cap);
             if constexpr (std::is_same<SpIn, NoSpmvIn>::value)
-                csr_spmv_kernel<In><<<(unsigned)L.items, NT, 0, st>>>(g, in, ws.nbuf, ws, pred, row);
+                csr_spmv_kernel<In><<<sgrid, NT, 0, st>>>(g, in, ws.nbuf, ws, pred, row);
             else
-                csr_spmv_kernel<SpIn><<<(unsigned)L.items, NT, 0, st>>>(g, spin, ws.nbuf, ws, pred, row);
+                csr_spmv_kernel<SpIn><<<sgrid, NT, 0, st>>>(g, spin, ws.nbuf, ws, pred, row);
         }
-        csr_chunk_sweep<In, Body><<<(unsigned)L.nch, NT, 0, st>>>(g, L, in, body, ws.nbuf, ws, cfg, phase, pred,
-                                                                 row);
+        csr_chunk_sweep<In, Body><<<(unsigned)std::min(L.nch, cap), NT, 0, st>>>(g, L, in, body, ws.nbuf, ws, cfg,
+                                                                               phase, pred, row);
     }
     return cuda_check("sweep launch");
 }

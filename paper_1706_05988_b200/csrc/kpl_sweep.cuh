@@ -55,7 +55,9 @@ stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wx = warp % L.wx, wy = warp / L.wx;
     const int TX = 32 * VX * L.wx, TY = L.wy;
-    const long long item = blockIdx.x;
+    // one item per CTA normally; rarely-active sweeps (replacement path) launch a
+    // small grid that strides over the items so an idle launch costs a few CTAs
+    for (long long item = blockIdx.x; item < L.items; item += gridDim.x) {
     const long long c = item / L.T;
     const int tile = (int)(item - c * L.T);
     const int tyi = tile / L.ntx, txi = tile - tyi * L.ntx;
@@ -210,6 +212,8 @@ stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int
         }
         complete_item<Q>(ws, cfg, L, phase, c, sred);
     }
+    __syncthreads();           // smem planes are restaged by the next item
+    }
 }
 
 template <class In, class Body>
@@ -308,7 +312,9 @@ csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long l
     if (ws.head && !pred_ok(ws.head, pred, row)) return;
     if (ws.head) in.setup(ws);
     const int tid = threadIdx.x;
-    const long long r0 = (long long)blockIdx.x * RB;
+    const long long nblk = (g.n + RB - 1) / RB;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const long long r0 = blk * RB;
     const long long r = r0 + tid;
     const bool ok = r < g.n;
     const long long rend = min(r0 + RB, g.n);
@@ -343,6 +349,7 @@ csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long l
         __syncthreads();
     }
     if (ok) out[r] = a;
+    }
 }
 
 template <class In, class Body>
@@ -356,7 +363,8 @@ csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ n
     body.setup(ws);
     in.setup(ws);
     const int tid = threadIdx.x;
-    const long long chunk = blockIdx.x;
+    __shared__ int s_last;
+    for (long long chunk = blockIdx.x; chunk < L.nch; chunk += gridDim.x) {
     const long long it0 = chunk * L.T;
     const int nit = (int)min((long long)L.T, L.items - it0);
     // software pipeline over the chunk's items: streams of item i+1 in flight while i computes
@@ -405,31 +413,34 @@ csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ n
 #pragma unroll
         for (int q = 0; q < Q; ++q) v[q] = (tid < nit) ? __dadd_rn(0.0, sitem[q][tid]) : 0.0;
         block_sum<Q>(v, sred);
-        __shared__ int s_last;
         const long long cg = ws.chunk_offset + chunk;
         if (tid == 0) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) ws.chunks[cg * NQ + q] = v[q];
         }
-        if (!ws.inline_final) return;
-        if (tid == 0) {
-            __threadfence();
-            const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
-            s_last = (prev == (unsigned)(L.nch - 1));
-            if (s_last) __threadfence();
-        }
-        __syncthreads();
-        if (!s_last) return;
-        double f[Q];
-        strided_sum<Q>(ws.chunks, ws.chunks_global, NQ, f, sred);
-        if (tid == 0) {
-            double full[NQ] = {0.0, 0.0, 0.0, 0.0};
+        if (ws.inline_final) {
+            if (tid == 0) {
+                __threadfence();
+                const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
+                s_last = (prev == (unsigned)(L.nch - 1));
+                if (s_last) __threadfence();
+            }
+            __syncthreads();
+            if (s_last) {          // the globally last chunk (necessarily this CTA's last)
+                double f[Q];
+                strided_sum<Q>(ws.chunks, ws.chunks_global, NQ, f, sred);
+                if (tid == 0) {
+                    double full[NQ] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int q = 0; q < Q; ++q) full[q] = f[q];
-            finalize(ws, cfg, phase, full);
-            ws.head->final_cnt = 0u;
-            __threadfence();
+                    for (int q = 0; q < Q; ++q) full[q] = f[q];
+                    finalize(ws, cfg, phase, full);
+                    ws.head->final_cnt = 0u;
+                    __threadfence();
+                }
+            }
         }
+    }
+    __syncthreads();
     }
 }
 
