@@ -15,5 +15,10 @@ from .solvers import (BreakdownError, DEFAULT_RR_THRESHOLD, IterationRecord, Sol
                       SolverConfig, SolverState, UNIT_ROUNDOFF, solve, solve_cg, solve_pcg,
                       solve_pcg_rr, solve_pcg_shifted, solve_pcg_var_shifted)
 from .ops import axpy, dot, norm2, spmv
+from .mmio import MatrixMarketError, read_matrix_market, write_matrix_market
+from .shift import (CoefficientHistory, ShiftSweep, amplification_factor, choose_shift,
+                    default_sigma_grid, margin_rule, matrix_2norm, propagation_matrix, select_shift)
+from .harness import (HISTORY_COLUMNS, RunConfig, build_preconditioner, emit_history, load_history,
+                      load_matrix, parse_sigma_grid, run_analyze_shift, run_solve)
 
 __version__ = "0.1.0"

@@ -227,10 +227,33 @@ def shift_selection():
     np.savez_compressed(os.path.join(HERE, "shift.npz"), **out)
 
 
+def formats():
+    """Reference history CSV/JSON and Matrix Market bytes (harness.py:99-130, mmio.py:103-122)."""
+    import io
+    from kpl import emit_history, write_matrix_market
+    out = {}
+    A = laplacian_2d(5, 4)
+    b = np.full(A.n, 1 / np.sqrt(A.n))
+    for tag, cfg in (("gaps", SolverConfig(method="pcg_sh", shift=1.0, max_iters=12, track_gaps=True)),
+                     ("plain", SolverConfig(method="pcg_rr", max_iters=25))):
+        res = solve(A, None, b, None, cfg)
+        out[f"{tag}_hist"] = hist_array(res)
+        for fmt in ("csv", "json"):
+            sink = io.StringIO()
+            emit_history(res.history, fmt, sink)
+            out[f"{tag}_{fmt}"] = np.frombuffer(sink.getvalue().encode("ascii"), dtype=np.uint8)
+    for tag, M in (("lap5x4", laplacian_2d(5, 4)), ("rspd6", random_spd(6, cond=30.0, seed=2))):
+        sink = io.BytesIO()
+        write_matrix_market(M, sink)
+        out[f"mm_{tag}"] = np.frombuffer(sink.getvalue(), dtype=np.uint8)
+        out.update(csr_arrays(M, f"mmA_{tag}"))
+    np.savez_compressed(os.path.join(HERE, "formats.npz"), **out)
+
+
 if __name__ == "__main__":
     print("reference kpl", kpl.__version__, "from", kpl.__file__)
     only = sys.argv[1:]
     for name, fn in (("kernels", kernels), ("solvers_small", solvers_small), ("config1", config1),
-                     ("jacobi_3d", jacobi_and_3d), ("shift", shift_selection)):
+                     ("jacobi_3d", jacobi_and_3d), ("shift", shift_selection), ("formats", formats)):
         if not only or name in only:
             fn()
