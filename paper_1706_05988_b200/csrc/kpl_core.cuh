@@ -56,7 +56,6 @@ enum Pred : int {
     PRED_RUNNING = 1,        // state == RUNNING
     PRED_FIRE = 2,           // state == RUNNING && fire  (pcg_rr replacement)
     PRED_ROW = 3,            // head.iter == row (explicit true-residual row)
-    PRED_CADENCE = 4,        // head.iter % 10 == 0 and state == RUNNING (graph mode)
 };
 
 struct Layout {               // identical on host and device
@@ -90,9 +89,6 @@ struct Cfg {                  // scalar view of kpl_cfg
 };
 
 // ------------------------------------------------------------- memory ops
-template <int V> struct Vec;
-template <> struct Vec<1> { using T = double; };
-template <> struct Vec<2> { using T = double2; };
 
 // streaming (evict-first) loads/stores for the vectors touched once per sweep
 template <int V>
@@ -380,7 +376,6 @@ __device__ __forceinline__ bool pred_ok(const WsHead *h, int pred, long long row
     case PRED_RUNNING: return h->state == KPL_ST_RUNNING;
     case PRED_FIRE: return h->state == KPL_ST_RUNNING && h->fire != 0;
     case PRED_ROW: return h->iter == row && h->state != KPL_ST_BREAKDOWN;
-    case PRED_CADENCE: return h->state == KPL_ST_RUNNING && (h->iter % 10) == 0;
     default: return true;
     }
 }

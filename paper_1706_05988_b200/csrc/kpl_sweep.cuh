@@ -8,11 +8,9 @@
 //    one-row y halo, and the body's streams for plane z+1 are prefetched into
 //    registers while plane z is computed.  One __syncthreads per plane.
 //
-//  * csr_sweep: one CTA per 256-row block.  The block's nonzeros are staged
-//    through shared memory in windows (coalesced loads of values/col_idx,
-//    gather of the input), then each thread sums its own row left to right
-//    from +0.0 -- the reference csr_matvec order (_kernels.py:44-52) -- and
-//    runs the body on that row.
+//  * csr_spmv_kernel + csr_chunk_sweep (CSR): the SpMV in the reference's
+//    csr_matvec order (_kernels.py:44-52), then the body's update + reductions
+//    one reduction chunk per CTA (see the block comment below).
 //
 // Both end with the same deterministic reduction: per-element accumulators
 // (sequential over z for stencils), per-thread pair sum (VX=2), warp xor
@@ -216,80 +214,6 @@ stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int
     }
 }
 
-template <class In, class Body>
-__global__ void __launch_bounds__(NT, 3)
-csr_sweep(CGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
-    constexpr int Q = Body::NQ;
-    constexpr int PER = CSR_WIN / NT;           // nonzeros staged per thread per window
-    __shared__ double sprod[Body::kStencil ? CSR_WIN : 1];
-    __shared__ double sred[NQ * NWARP];
-    if (!pred_ok(ws.head, pred, row)) return;
-    body.setup(ws);
-    in.setup(ws);
-
-    const int tid = threadIdx.x;
-    const long long item = blockIdx.x;
-    const long long r0 = item * RB;
-    const long long r = r0 + tid;
-    const bool ok = r < g.n;
-    // the body's own-row streams do not depend on the SpMV: issue them first
-    typename Body::template Regs<1> R;
-    if (ok) body.template load<1>(r, R);
-    double n[1] = {0.0};
-    double cen[1] = {0.0};
-    if constexpr (Body::kStencil) {
-        const long long rend = min(r0 + RB, g.n);
-        const long long k0 = __ldg(g.row_ptr + r0), k1 = __ldg(g.row_ptr + rend);
-        long long lo = 0, hi = 0;
-        if (ok) { lo = __ldg(g.row_ptr + r); hi = __ldg(g.row_ptr + r + 1); }
-        if (ok) in.template raw<1>(in.base(), r, cen);
-        double a = 0.0;
-        for (long long wk = k0; wk < k1; wk += CSR_WIN) {
-            const long long we = min(wk + (long long)CSR_WIN, k1);
-            // stage: all index/value loads first, then all gathers (MLP), then products
-            int col[PER];
-            double val[PER], raw[PER];
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const long long kk = wk + tid + (long long)j * NT;
-                col[j] = 0; val[j] = 0.0;
-                if (kk < we) { col[j] = __ldcs(g.col_idx + kk); val[j] = __ldcs(g.values + kk); }
-            }
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const long long kk = wk + tid + (long long)j * NT;
-                raw[j] = 0.0;
-                if (kk < we) { double t[1]; in.template raw<1>(in.base(), col[j], t); raw[j] = t[0]; }
-            }
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const long long kk = wk + tid + (long long)j * NT;
-                if (kk < we) sprod[kk - wk] = __dmul_rn(val[j], in.xf(raw[j], col[j]));
-            }
-            __syncthreads();
-            const long long a0 = max(lo, wk), a1 = min(hi, we);
-            for (long long kk = a0; kk < a1; ++kk) a = __dadd_rn(a, sprod[kk - wk]);   // csr_matvec order
-            __syncthreads();
-        }
-        n[0] = a;
-    }
-    double acc[Q > 0 ? Q : 1][1];
-#pragma unroll
-    for (int q = 0; q < (Q > 0 ? Q : 1); ++q) acc[q][0] = 0.0;
-    if (ok) body.template compute<1>(r, R, n, cen, acc);
-    if constexpr (Q > 0) {
-        double t[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) t[q] = acc[q][0];
-        block_sum<Q>(t, sred);
-        if (tid == 0) {
-#pragma unroll
-            for (int q = 0; q < Q; ++q) ws.items[item * NQ + q] = t[q];
-        }
-        complete_item<Q>(ws, cfg, L, phase, item / L.T, sred);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // CSR, split form (the production CSR path).
 //
@@ -303,7 +227,8 @@ csr_sweep(CGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pre
 //                    the body's update for every row of the chunk with n read
 //                    back from memory, item partials kept in shared memory, the
 //                    chunk fold (level 3) done in-CTA, one completion atomic per
-//                    chunk.  Same items, same tree: bit-identical to csr_sweep.
+//                    chunk.  The item (256 rows) and chunk trees are the ones
+//                    oracle/gpu_order.py emulates.
 template <class In>
 __global__ void __launch_bounds__(NT, 6)
 csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
