@@ -136,9 +136,16 @@ def run_ours(args):
     from paper_1706_05988_b200.solvers import _Solve
 
     rank, world, local = dist_env()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink; KPL_DIST_BACKEND=gloo runs the same multi-process
+        # path with several ranks on one GPU (plumbing checks only)
+        backend = os.environ.get("KPL_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         return run_distributed(args, rank, world, local)
     dev = torch.device("cuda", local)
 
@@ -342,7 +349,7 @@ def run_distributed(args, rank, world, local):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated operator and rhs; no dataset)",
         "config": {"workload": WORKLOAD, "n": n, "iterations_per_step": res.iterations,
-                   "parallelism": f"z-slab x{world} (NCCL halo send/recv + chunk all-gather)",
+                   "parallelism": f"z-slab x{world} ({dist.get_backend()} halo send/recv + chunk all-gather)",
                    "l2": "no flush: per-rank vectors >> 126 MB L2"},
         "hbm_gbs": hbm, "hbm_frac_of_measured": hbm / peak / world,
         "e2e": {"value": res.iterations * args.steps / t_e2e, "unit": UNIT,

@@ -328,41 +328,71 @@ class TorchComm:
         self.size = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self._counts = None
+        # gloo moves CUDA tensors for collectives but not point-to-point: stage
+        # those through host memory (used to run the multi-process path on a
+        # single GPU; NCCL is the production backend)
+        self.stage_p2p = dist.get_backend(group) == "gloo"
+
+    def _p2p(self, sends, recvs):
+        """sends/recvs: lists of (tensor, peer)."""
+        dist = self.dist
+        if self.stage_p2p:
+            host_s = [(t.cpu(), q) for t, q in sends]
+            host_r = [(t.new_empty(t.shape, device="cpu"), q) for t, q in recvs]
+            ops = [dist.P2POp(dist.isend, t, q, self.group) for t, q in host_s]
+            ops += [dist.P2POp(dist.irecv, t, q, self.group) for t, q in host_r]
+            if ops:
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+            for (dst, _), (src, _) in zip(recvs, host_r):
+                dst.copy_(src)
+            return
+        ops = [dist.P2POp(dist.isend, t, q, self.group) for t, q in sends]
+        ops += [dist.P2POp(dist.irecv, t, q, self.group) for t, q in recvs]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
 
     def local_ranks(self):
         return [self.rank]
 
     def exchange(self, states, name):
-        dist = self.dist
         (s,) = states
-        ops = []
+        sends, recvs = [], []
         if isinstance(s, _SlabState):
             lo, first, last, hi = s.planes(name)
             if s.rank > 0:
-                ops.append(dist.P2POp(dist.isend, first.contiguous(), s.rank - 1, self.group))
-                ops.append(dist.P2POp(dist.irecv, lo, s.rank - 1, self.group))
+                sends.append((first, s.rank - 1))
+                recvs.append((lo, s.rank - 1))
             if s.rank < self.size - 1:
-                ops.append(dist.P2POp(dist.isend, last.contiguous(), s.rank + 1, self.group))
-                ops.append(dist.P2POp(dist.irecv, hi, s.rank + 1, self.group))
+                sends.append((last, s.rank + 1))
+                recvs.append((hi, s.rank + 1))
         else:
             for q, idx in s.send_idx.items():          # pack the rows each peer needs
                 _gather(idx, s.interior(name), s.send_buf[q])
-                ops.append(dist.P2POp(dist.isend, s.send_buf[q], q, self.group))
+                sends.append((s.send_buf[q], q))
             for q in s.recv:
-                ops.append(dist.P2POp(dist.irecv, s.ghost(name, q), q, self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+                recvs.append((s.ghost(name, q), q))
+        self._p2p(sends, recvs)
 
     def allgather(self, states):
         (s,) = states
         t = D.torch()
         if self._counts is None:
-            c = t.tensor([s.chunks_local], dtype=t.int64, device=s.table.device)
+            dev = "cpu" if self.stage_p2p else s.table.device
+            c = t.tensor([s.chunks_local], dtype=t.int64, device=dev)
             allc = [t.zeros_like(c) for _ in range(self.size)]
             self.dist.all_gather(allc, c, group=self.group)
             self._counts = [int(v.item()) for v in allc]
         counts = self._counts
+        if self.stage_p2p:                       # gloo: host-staged, equal-size (padded) all-gather
+            mx = max(counts)
+            mine = t.zeros(4 * mx, dtype=t.float64)
+            mine[:4 * counts[self.rank]].copy_(s.table_local.cpu())
+            parts = [t.zeros(4 * mx, dtype=t.float64) for _ in counts]
+            self.dist.all_gather(parts, mine, group=self.group)
+            s.table.copy_(t.cat([p[:4 * cq] for p, cq in zip(parts, counts)]))
+            return
         if all(c == counts[0] for c in counts):
             # in-place all-gather: this rank's slice sits at offset rank*count
             self.dist.all_gather_into_tensor(s.table, s.table_local.clone(), group=self.group)

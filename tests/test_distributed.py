@@ -319,3 +319,78 @@ def test_gloo_row_ghost_exchange():
         assert p.exitcode == 0
     for rank, ok, ng in res:
         assert ok and ng > 0, (rank, ng)
+
+
+def _gloo_gpu_worker(rank, world, port, q, kind):
+    """One rank of a real multi-process solve: gloo for plumbing, all ranks on cuda:0."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1706_05988_b200 as K
+        from paper_1706_05988_b200 import problems
+        from paper_1706_05988_b200.distributed import RowPlan, SlabPlan, solve_distributed
+        torch.cuda.set_device(0)
+        if kind == "slab":
+            A = K.Stencil3D(64, 24, 32)
+            b = np.random.default_rng(2).normal(size=A.n)
+            plan = SlabPlan(64, 24, 32, world, 4)
+            cfg = K.SolverConfig(method="pcg_sh", shift=2.3, max_iters=60)
+            M = None
+            res = solve_distributed(A, M, b[plan.local_slice(rank)], None, cfg, zc=4)
+        else:
+            A = problems.banded_spd(20000, seed=0, band=2000)
+            M = K.make_jacobi(A)
+            b = np.random.default_rng(1).standard_normal(A.n)
+            plan = RowPlan(A, world)
+            cfg = K.SolverConfig(method="pcg_sh", shift=0.41, max_iters=60, rtol=1e-10)
+            res = solve_distributed(A, M, b[plan.local_slice(rank)], None, cfg)
+        q.put((rank, res.iterations, [r.alpha for r in res.history], res.x[0].cpu().numpy().tobytes()))
+    except Exception as exc:                      # report, don't hang the parent
+        q.put((rank, "error", repr(exc), b""))
+    finally:
+        dist.destroy_process_group()
+
+
+@gpu
+@pytest.mark.parametrize("kind", ["slab", "rows"])
+def test_multiprocess_gloo_on_one_gpu_bitwise(kind):
+    """TorchComm + the sweep-level C ABI in real separate processes (2 ranks
+    sharing cuda:0, gloo for the exchanges); bit-identical to one GPU."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200 import problems
+    from paper_1706_05988_b200.distributed import RowPlan, SlabPlan
+    from paper_1706_05988_b200.solvers import _Solve
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_gloo_gpu_worker, args=(r, 2, port, q, kind)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(2):
+        r, its, alphas, xb = q.get(timeout=300)
+        assert its != "error", alphas
+        out[r] = (its, alphas, xb)
+    for p in procs:
+        p.join(timeout=120)
+    if kind == "slab":
+        A = K.Stencil3D(64, 24, 32)
+        b = np.random.default_rng(2).normal(size=A.n)
+        ref = _Solve(A, None, b, None, K.SolverConfig(method="pcg_sh", shift=2.3, max_iters=60), zc=4).run()
+        plan = SlabPlan(64, 24, 32, 2, 4)
+    else:
+        A = problems.banded_spd(20000, seed=0, band=2000)
+        b = np.random.default_rng(1).standard_normal(A.n)
+        ref = K.solve(A, K.make_jacobi(A), b, None,
+                      K.SolverConfig(method="pcg_sh", shift=0.41, max_iters=60, rtol=1e-10))
+        plan = RowPlan(A, 2)
+    for r in range(2):
+        its, alphas, xb = out[r]
+        assert its == ref.iterations
+        assert alphas == [h.alpha for h in ref.history]
+        assert xb == ref.x[plan.local_slice(r)].tobytes()
