@@ -167,6 +167,12 @@ int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
    multiple of 10.                                                          */
 int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
                        int64_t first, int64_t count, void *workspace, void *stream);
+/* Same as kpl_solver_iterate, as ONE cooperative (persistent) launch with a
+   grid barrier between passes -- for small problems where per-iteration
+   launch latency dominates.  Single-GPU stencil p-CG / p-CG-sh / p-CG-var-sh
+   without track_gaps (KPL_EUNSUPPORTED otherwise).  Bit-identical results.  */
+int kpl_solver_iterate_persistent(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
+                                  int64_t first, int64_t count, void *workspace, void *stream);
 /* Classic CG in two halves so a host callback can observe the record
    point (solvers.py:286-287): pass 1 = true-residual cadence + p, s = A p,
    delta, record; pass 2 = x, r, u updates and the next head.               */

@@ -73,6 +73,8 @@ _SIGS = {
                                ctypes.POINTER(KplVecs), _p, _p, _p]),
     "kpl_solver_iterate": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
                                   ctypes.POINTER(KplVecs), _i64, _i64, _p, _p]),
+    "kpl_solver_iterate_persistent": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
+                                             ctypes.POINTER(KplVecs), _i64, _i64, _p, _p]),
     "kpl_solver_cg_pass": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
                                   ctypes.POINTER(KplVecs), _i64, _i32, _p, _p]),
     "kpl_solver_finish": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),

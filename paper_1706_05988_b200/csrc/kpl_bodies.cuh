@@ -18,10 +18,12 @@ namespace kpl {
 
 enum Sel : int { SEL_FIXED = 0, SEL_ITER = 1, SEL_ITER1 = 2 };
 
+// Scalars and the iteration counter are read through L2 (__ldcg): inside a
+// persistent kernel they were written by another CTA after a grid barrier.
 __device__ __forceinline__ const double *pick(const WsHead *h, int sel, const double *a0,
                                               const double *a1) {
     if (sel == SEL_FIXED) return a0;
-    const long long par = (h->iter + (sel == SEL_ITER1 ? 1 : 0)) & 1;
+    const long long par = (__ldcg(&h->iter) + (sel == SEL_ITER1 ? 1 : 0)) & 1;
     return par ? a1 : a0;
 }
 
@@ -46,9 +48,19 @@ struct InVec {
     double c;
     const double *dinv;
     const double *a;
+    int coherent;          // 1: read through L2 (the vector was written earlier in this kernel)
     __device__ void setup(const Ws &ws) { a = pick(ws.head, sel, a0, a1); }
     __device__ const double *base() const { return a; }
     template <int V> __device__ void raw(const double *p, long long k, double (&o)[V]) const {
+        if (coherent) {
+            if constexpr (V == 2) {
+                const double2 t = __ldcg(reinterpret_cast<const double2 *>(p + k));
+                o[0] = t.x; o[1] = t.y;
+            } else {
+                o[0] = __ldcg(p + k);
+            }
+            return;
+        }
         ld_ro<V>(p, k, o);
     }
     __device__ double xf(double r, long long k) const {
@@ -258,10 +270,10 @@ struct BodyPcgIter {
         if constexpr (PC != KPL_PC_IDENTITY) { sm2(S, 5, cs, R.u); sm2(S, 6, cs, R.q); sm2(S, 7, cs, R.p); }
     }
     __device__ void setup(const Ws &ws) {
-        alpha = ws.head->alpha;
-        beta = ws.head->beta;
+        alpha = __ldcg(&ws.head->alpha);
+        beta = __ldcg(&ws.head->beta);
         if constexpr (VAR) {
-            const long long i = ws.head->iter;
+            const long long i = __ldcg(&ws.head->iter);
             const double sp = schedule[i];
             sigma = schedule[i + 1];                    // sigma_cur; also the next delta's shift
             dsig = __dsub_rn(sigma, sp);                // solvers.py:481

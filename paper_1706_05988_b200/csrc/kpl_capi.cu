@@ -179,6 +179,7 @@ template <int PC>
 InVec<PC> in_vec(const kpl_op *op, const double *a0, const double *a1, int sel) {
     InVec<PC> in;
     in.a0 = a0; in.a1 = a1; in.sel = sel; in.c = op->pc_const; in.dinv = op->inv_diag; in.a = a0;
+    in.coherent = 0;
     return in;
 }
 
@@ -310,6 +311,8 @@ __global__ void head_init_kernel(WsHead *h, double *hist, long long nrows, unsig
         h->gamma_prev = 0.0;    // solvers.py:382
         h->alpha_prev = 1.0;    // solvers.py:383
         h->final_cnt = 0u;
+        h->bar_cnt = 0u;
+        h->bar_gen = 0u;
         h->cg_gamma = 0.0;
     }
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
@@ -763,6 +766,61 @@ int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v,
         }
     }
     return KPL_OK;
+}
+
+// Persistent cooperative solve of `count` iterations (small stencil problems,
+// pipelined methods without gaps/replacement): see persistent_pipelined.
+int kpl_solver_iterate_persistent(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t first,
+                                  int64_t count, void *workspace, void *stream) {
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
+    if (rc != KPL_OK) return rc;
+    const int m = c.cfg.method;
+    if (op->kind != KPL_OP_STENCIL || op->chunks_global > 0 || c.cfg.track_gaps ||
+        !(m == KPL_M_PCG || m == KPL_M_PCG_SH || m == KPL_M_PCG_VAR_SH))
+        return fail(KPL_EUNSUPPORTED, "persistent solve: single-GPU stencil p-CG / p-CG-sh / var-sh only");
+    if (count <= 0) return KPL_OK;
+    const Layout &L = c.L;
+    SGeo g{op->nx, op->ny, op->nz, op->diag, op->halo_lo, op->halo_hi, op->zhalo};
+    BodyTrue tb;
+    tb.b = v->b;
+    auto in_x = in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED);
+    in_x.coherent = 1;
+    return with_pc(op, [&](auto pc) -> int {
+        constexpr int PC = decltype(pc)::value;
+        auto go = [&](auto body) -> int {
+            using B = decltype(body);
+            auto in_w = in_vec<PC>(op, v->w0, v->w1, SEL_ITER);
+            in_w.coherent = 1;
+            body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
+            body.s = v->s; body.t = v->t; body.p = v->p; body.w0 = v->w0; body.w1 = v->w1;
+            body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = c.sigma; body.dsig = 0.0;
+            body.schedule = c.cfg.schedule; body.want_xi = 0; body.mout = nullptr;
+            body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
+            void *args[] = {&g, const_cast<Layout *>(&L), &in_w, &body, &in_x, &tb,
+                            const_cast<Ws *>(&c.ws), const_cast<Cfg *>(&c.cfg), &first, &count};
+            int nb = 0, dev = 0;
+            cudaGetDevice(&dev);
+            int sms = kSMs;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (L.vx == 2) {
+                auto kern = persistent_pipelined<2, decltype(in_w), B, decltype(in_x)>;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, 0);
+                const unsigned grid = (unsigned)std::max(1LL, std::min(L.items, (long long)nb * sms));
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                cudaLaunchCooperativeKernel((void *)kern, grid, NT, args, 0, c.st);
+            } else {
+                auto kern = persistent_pipelined<1, decltype(in_w), B, decltype(in_x)>;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, 0);
+                const unsigned grid = (unsigned)std::max(1LL, std::min(L.items, (long long)nb * sms));
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                cudaLaunchCooperativeKernel((void *)kern, grid, NT, args, 0, c.st);
+            }
+            return cuda_check("persistent launch");
+        };
+        if (m == KPL_M_PCG_VAR_SH) return go(BodyPcgIter<PC, true>());
+        return go(BodyPcgIter<PC, false>());
+    });
 }
 
 int kpl_solver_cg_pass(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t j, int32_t pass,

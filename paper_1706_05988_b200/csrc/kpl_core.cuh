@@ -30,7 +30,7 @@ struct WsHead {
     double cg_gamma, cg_beta, cg_rnorm, cg_alpha; // classic CG head -> delta
     long long cg_last, _cg_pad;
     double dsig_pad[4];
-    unsigned int final_cnt, _cnt_pad[7];
+    unsigned int final_cnt, bar_cnt, bar_gen, _cnt_pad[5];   // completion count; grid barrier
 };
 static_assert(sizeof(WsHead) <= 1024, "head too large");
 
@@ -372,10 +372,12 @@ __device__ void finalize(const Ws &ws, const Cfg &cfg, int phase, const double (
 
 // Per-kernel uniform predicate.
 __device__ __forceinline__ bool pred_ok(const WsHead *h, int pred, long long row) {
+    if (pred == PRED_ALWAYS) return true;          // (plain spmv launches carry no workspace)
+    const long long state = __ldcg(&h->state);
     switch (pred) {
-    case PRED_RUNNING: return h->state == KPL_ST_RUNNING;
-    case PRED_FIRE: return h->state == KPL_ST_RUNNING && h->fire != 0;
-    case PRED_ROW: return h->iter == row && h->state != KPL_ST_BREAKDOWN;
+    case PRED_RUNNING: return state == KPL_ST_RUNNING;
+    case PRED_FIRE: return state == KPL_ST_RUNNING && __ldcg(&h->fire) != 0;
+    case PRED_ROW: return __ldcg(&h->iter) == row && state != KPL_ST_BREAKDOWN;
     default: return true;
     }
 }

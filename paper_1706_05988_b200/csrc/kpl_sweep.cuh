@@ -39,14 +39,16 @@ struct CGeo {
 constexpr int SMEM_PLANE = 1548;
 constexpr int CSR_WIN = 2048;      // staged nonzeros per window
 
+// One pass of a stencil sweep over all items (grid-stride), callable from the
+// one-launch-per-sweep kernel below and from the persistent solver kernel.
+// `spbuf` (2 * SMEM_PLANE doubles) and `sred` (NQ * NWARP) are the caller's
+// shared memory, so several passes in one kernel share it.
 template <int VX, class In, class Body>
-__global__ void __launch_bounds__(NT, 2)
-stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
+__device__ __forceinline__ void stencil_pass(const SGeo &g, const Layout &L, In in, Body body, const Ws &ws,
+                                             const Cfg &cfg, int phase, double *spbuf, double *sred) {
     constexpr int Q = Body::NQ;
-    __shared__ __align__(16) double sp[Body::kStencil ? 2 : 1][Body::kStencil ? SMEM_PLANE : 2];
-    __shared__ double sred[NQ * NWARP];
+    double (*sp)[SMEM_PLANE] = reinterpret_cast<double (*)[SMEM_PLANE]>(spbuf);
 
-    if (!pred_ok(ws.head, pred, row)) return;
     body.setup(ws);
     in.setup(ws);
 
@@ -211,6 +213,60 @@ stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int
         complete_item<Q>(ws, cfg, L, phase, c, sred);
     }
     __syncthreads();           // smem planes are restaged by the next item
+    }
+}
+
+template <int VX, class In, class Body>
+__global__ void __launch_bounds__(NT, 2)
+stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
+    __shared__ __align__(16) double sp[Body::kStencil ? 2 * SMEM_PLANE : 2];
+    __shared__ double sred[NQ * NWARP];
+    if (!pred_ok(ws.head, pred, row)) return;
+    stencil_pass<VX, In, Body>(g, L, in, body, ws, cfg, phase, sp, sred);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent solver for small stencil problems: one cooperative launch runs
+// up to `count` p-CG(-sh) iterations; a grid barrier replaces the kernel
+// boundary after every pass (the last CTA's scalar epilogue must be visible
+// before anybody reads alpha/beta).  Same passes, items and trees as the
+// per-iteration launches, so results are bit-identical.  Stencil-input loads
+// go through L2 (InVec::coherent) because neighbours' values were written
+// earlier in the same kernel.
+__device__ __forceinline__ void grid_sync(WsHead *h) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = atomicAdd(&h->bar_gen, 0u);
+        __threadfence();
+        if (atomicAdd(&h->bar_cnt, 1u) == gridDim.x - 1) {
+            atomicExch(&h->bar_cnt, 0u);
+            __threadfence();
+            atomicAdd(&h->bar_gen, 1u);
+        } else {
+            volatile unsigned *g = &h->bar_gen;          // poll through L2 without atomics
+            while (*g == gen) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int VX, class InW, class BodyIt, class InX>
+__global__ void __launch_bounds__(NT, 2)
+persistent_pipelined(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue tbody, Ws ws, Cfg cfg,
+                     long long first, long long count) {
+    __shared__ __align__(16) double sp[2 * SMEM_PLANE];
+    __shared__ double sred[NQ * NWARP];
+    for (long long j = first; j < first + count; ++j) {
+        if (__ldcg(&ws.head->state) != KPL_ST_RUNNING) break;     // uniform: read after a barrier
+        if (j % 10 == 0) {                                           // true-residual cadence (row j)
+            if (__ldcg(&ws.head->iter) == j)
+                stencil_pass<VX, InX, BodyTrue>(g, L, in_x, tbody, ws, cfg, PH_TRUE, sp, sred);
+            grid_sync(ws.head);
+        }
+        stencil_pass<VX, InW, BodyIt>(g, L, in_w, body, ws, cfg, PH_PIPE, sp, sred);
+        grid_sync(ws.head);
     }
 }
 

@@ -163,7 +163,13 @@ class SolverState:
 class _Solve:
     """One solve: device vectors, workspace, and the host enqueue loop."""
 
-    def __init__(self, A, M, b, x0, cfg: SolverConfig, *, zc=0, vx=0, chunk_blocks=0, slab_view=False):
+    # stencil problems up to this size run as persistent cooperative launches
+    # (one launch per chunk of iterations, grid barriers instead of kernel
+    # boundaries): there the per-iteration launch latency, not HBM, dominates
+    PERSISTENT_MAX_N = 1 << 20
+
+    def __init__(self, A, M, b, x0, cfg: SolverConfig, *, zc=0, vx=0, chunk_blocks=0, slab_view=False,
+                 persistent=None):
         self.device = dev = D.require_cuda()
         t = D.torch()
         self.cfg = cfg
@@ -206,6 +212,10 @@ class _Solve:
         self.hist_off = lib.kpl_history_offset(self.op)
         self.reps_off = lib.kpl_replacements_offset(self.op, cfg.max_iters)
         self.status = _lib.KplStatus()
+        if persistent is None:
+            persistent = (self.dm.kind == _lib.KPL_OP_STENCIL and n <= self.PERSISTENT_MAX_N
+                          and cfg.method in ("pcg", "pcg_sh", "pcg_var_sh") and not cfg.track_gaps)
+        self.persistent = bool(persistent)
         # classic CG records row i in the first half of pass i, so the final
         # row max_iters needs one more pass than the pipelined solvers
         self.limit = cfg.max_iters + (1 if cfg.method == "cg" else 0)
@@ -222,8 +232,9 @@ class _Solve:
         count = min(count, self.limit - self.issued)
         if count <= 0:
             return
-        _lib.check(lib.kpl_solver_iterate(self.op, self.kcfg, self.vecs, self.issued, count,
-                                          D.ptr(self.ws), D.stream_handle()), "solver iterate")
+        fn = lib.kpl_solver_iterate_persistent if self.persistent else lib.kpl_solver_iterate
+        _lib.check(fn(self.op, self.kcfg, self.vecs, self.issued, count, D.ptr(self.ws),
+                      D.stream_handle()), "solver iterate")
         self.issued += count
 
     def read_status(self):

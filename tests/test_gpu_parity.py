@@ -339,3 +339,21 @@ def test_var_shift_jacobi_csr_bitwise():
     oA = O.as_oracle_operator(A)
     ores = O.solve(oA, O.make_jacobi(oA), b, None, O.Config(**cfg), dot=gpu_dot(A))
     assert same_bits(hist11(res), np.ascontiguousarray(ores.history)) and same_bits(res.x, ores.x)
+
+
+@pytest.mark.parametrize("shape,jac,method", [((200, 200), False, "pcg_sh"), ((37, 23), False, "pcg"),
+                                              ((64, 48), True, "pcg_sh"), ((24, 20, 16), False, "pcg_var_sh")])
+def test_persistent_solver_bitwise(shape, jac, method):
+    """The persistent cooperative path (small stencils) == per-iteration launches, bit for bit."""
+    from paper_1706_05988_b200.solvers import _Solve
+    A = K.Stencil2D(*shape) if len(shape) == 2 else K.Stencil3D(*shape)
+    M = K.make_jacobi(A) if jac else None
+    b = np.random.default_rng(4).normal(size=A.n)
+    extra = {"shift": 1.1} if method == "pcg_sh" else {}
+    if method == "pcg_var_sh":
+        extra = {"shift_schedule": tuple(0.02 * k for k in range(301))}
+    cfg = K.SolverConfig(method=method, max_iters=300, rtol=1e-10, **extra)
+    r1 = _Solve(A, M, b, None, cfg, persistent=True).run()
+    r2 = _Solve(A, M, b, None, cfg, persistent=False).run()
+    assert r1.iterations == r2.iterations
+    assert same_bits(hist11(r1), hist11(r2)) and same_bits(r1.x, r2.x)
