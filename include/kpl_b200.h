@@ -74,7 +74,19 @@ typedef struct kpl_op {
        (0 = single GPU: the last CTA finalises inline)                       */
     int64_t chunk_offset;
     int64_t chunks_global;
+    /* reduction order of every dot product / norm (single GPU):
+       KPL_ORDER_TREE     the fixed tile/chunk tree (default, bandwidth-bound)
+       KPL_ORDER_BLOCKED8 the reference's blocked_dot order exactly
+                          (_kernels.py:16-41: 8 sequential lanes over k mod 8,
+                          lanes folded pairwise, tail added last): results are
+                          bit-identical to the reference's solvers, at the cost
+                          of a sequential n/8-long fold after each sweep      */
+    int32_t order;
+    int32_t _reserved;
 } kpl_op;
+
+#define KPL_ORDER_TREE      0
+#define KPL_ORDER_BLOCKED8  1
 
 /* ---- solver configuration (mirror of SolverConfig, solvers.py:60-86) ---- */
 #define KPL_M_CG         0

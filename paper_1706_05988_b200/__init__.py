@@ -15,6 +15,7 @@ from .solvers import (BreakdownError, DEFAULT_RR_THRESHOLD, IterationRecord, Sol
                       SolverConfig, SolverState, UNIT_ROUNDOFF, solve, solve_cg, solve_pcg,
                       solve_pcg_rr, solve_pcg_shifted, solve_pcg_var_shifted)
 from .ops import axpy, dot, norm2, spmv
+from .device import get_reduction_order, reduction_order, set_reduction_order
 from .mmio import MatrixMarketError, read_matrix_market, write_matrix_market
 from .shift import (CoefficientHistory, ShiftSweep, amplification_factor, choose_shift,
                     default_sigma_grid, margin_rule, matrix_2norm, propagation_matrix, select_shift)

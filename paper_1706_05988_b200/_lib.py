@@ -22,6 +22,7 @@ KPL_PC_IDENTITY, KPL_PC_JACOBI_CONST, KPL_PC_JACOBI_VEC = 0, 1, 2
 KPL_M_CG, KPL_M_PCG, KPL_M_PCG_SH, KPL_M_PCG_VAR_SH, KPL_M_PCG_RR = 0, 1, 2, 3, 4
 KPL_ST_RUNNING, KPL_ST_DONE, KPL_ST_BREAKDOWN = 0, 1, 2
 KPL_HIST_COLS = 10
+KPL_ORDER_TREE, KPL_ORDER_BLOCKED8 = 0, 1
 (KPL_SW_BNORM, KPL_SW_INIT_R, KPL_SW_INIT_W, KPL_SW_ITER, KPL_SW_TRUE, KPL_SW_CG_P, KPL_SW_CG_X,
  KPL_SW_RR_R, KPL_SW_RR_W, KPL_SW_RR_S, KPL_SW_RR_Z,
  KPL_SW_GAP_F, KPL_SW_GAP_G, KPL_SW_GAP_H, KPL_SW_GAP_J) = range(1, 16)
@@ -38,7 +39,7 @@ class KplOp(ctypes.Structure):
                 ("zc", _i32), ("vx", _i32), ("halo_lo", _p), ("halo_hi", _p),
                 ("row_ptr", _p), ("col_idx", _p), ("values", _p), ("nnz", _i64),
                 ("chunk_blocks", _i32), ("zhalo", _i32), ("pc_const", _d), ("inv_diag", _p),
-                ("chunk_offset", _i64), ("chunks_global", _i64)]
+                ("chunk_offset", _i64), ("chunks_global", _i64), ("order", _i32), ("_reserved", _i32)]
 
 
 class KplCfg(ctypes.Structure):

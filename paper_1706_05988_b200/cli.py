@@ -17,6 +17,7 @@ import sys
 
 import numpy as np
 
+from .device import reduction_order
 from .harness import RunConfig, load_matrix, parse_sigma_grid, run_analyze_shift, run_solve
 from .mmio import write_matrix_market
 from .shift import default_sigma_grid
@@ -38,7 +39,8 @@ def cmd_solve(a) -> int:
     cfg = RunConfig(matrix_source=a.matrix, rhs_mode=a.rhs.replace("-", "_"), precond=a.precond,
                     ic_eta=a.ic_shift, solver=solver, output_format=a.format,
                     output_path=a.history, seed=a.seed)
-    res, _, _, _ = run_solve(cfg)
+    with reduction_order(a.reduction_order):
+        res, _, _, _ = run_solve(cfg)
     last = res.history[-1]
     print(f"method={a.method} n-iterations={res.iterations} converged={res.converged}")
     print(f"recursive residual norm: {last.rnorm_recursive:.6e}")
@@ -97,6 +99,9 @@ def main(argv=None) -> int:
     s.add_argument("--history", metavar="PATH")
     s.add_argument("--format", choices=["csv", "json"], default="csv")
     s.add_argument("--seed", type=int, default=0)
+    s.add_argument("--reduction-order", choices=["tree", "reference"], default="tree",
+                   help="dot-product order: the device tree (default) or the reference's "
+                        "blocked order (bit-identical to the reference's output)")
     s.set_defaults(func=cmd_solve)
     an = sub.add_parser("analyze-shift", help="sweep the amplification factor over shifts")
     an.add_argument("--history", required=True, metavar="PATH")

@@ -119,18 +119,19 @@ struct BodySpmv {
 struct BodyDot {
     static constexpr int NQ = 1;
     static constexpr bool kStencil = false;
+    Sink sk;              // reference-order product sink
     const double *a, *b;
     template <int V> struct Regs { double a[V], b[V]; };
-    __device__ void setup(const Ws &) {}
+    __device__ void setup(const Ws &ws) { sk.set(ws); }
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
         ld_cs<V>(a, k, R.a);
         ld_cs<V>(b, k, R.b);
     }
     template <int V>
-    __device__ void compute(long long, const Regs<V> &R, const double (&)[V], const double (&)[V],
+    __device__ void compute(long long k, const Regs<V> &R, const double (&)[V], const double (&)[V],
                             double (&acc)[1][V]) const {
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(R.a[v], R.b[v]));
+        for (int v = 0; v < V; ++v) accp(acc, 0, v, sk, k, __dmul_rn(R.a[v], R.b[v]));
     }
 };
 
@@ -140,6 +141,7 @@ template <int PC>
 struct BodyInitR {
     static constexpr int NQ = 3;
     static constexpr bool kStencil = true;
+    Sink sk;              // reference-order product sink
     const double *b;
     double *x, *r, *u;
     const double *dinv;
@@ -147,7 +149,7 @@ struct BodyInitR {
     int copy_x;
     template <int V> struct Regs { double b[V], d[V]; };
     static constexpr int kTmaStreams = 1;                 // b
-    __device__ void setup(const Ws &) {}
+    __device__ void setup(const Ws &ws) { sk.set(ws); }
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
         ld_cs<V>(b, k, R.b);
         if constexpr (PC == KPL_PC_JACOBI_VEC) ld_cs<V>(dinv, k, R.d);
@@ -163,9 +165,9 @@ struct BodyInitR {
             if constexpr (PC == KPL_PC_IDENTITY) uu[v] = rr[v];
             else if constexpr (PC == KPL_PC_JACOBI_CONST) uu[v] = __dmul_rn(rr[v], c);
             else uu[v] = __dmul_rn(rr[v], R.d[v]);
-            acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(xin[v], xin[v]));
-            acc[1][v] = __dadd_rn(acc[1][v], __dmul_rn(rr[v], rr[v]));
-            acc[2][v] = __dadd_rn(acc[2][v], __dmul_rn(rr[v], uu[v]));
+            accp(acc, 0, v, sk, k, __dmul_rn(xin[v], xin[v]));
+            accp(acc, 1, v, sk, k, __dmul_rn(rr[v], rr[v]));
+            accp(acc, 2, v, sk, k, __dmul_rn(rr[v], uu[v]));
         }
         st_cs<V>(r, k, rr);
         if constexpr (PC != KPL_PC_IDENTITY) st_cs<V>(u, k, uu);
@@ -177,19 +179,20 @@ struct BodyInitR {
 struct BodyTrue {
     static constexpr int NQ = 1;
     static constexpr bool kStencil = true;
+    Sink sk;              // reference-order product sink
     const double *b;
     template <int V> struct Regs { double b[V]; };
     static constexpr int kTmaStreams = 1;                 // b
-    __device__ void setup(const Ws &) {}
+    __device__ void setup(const Ws &ws) { sk.set(ws); }
     template <int V> __device__ void load(long long k, Regs<V> &R) const { ld_cs<V>(b, k, R.b); }
     __device__ void load_tma(const double *S, int cs, Regs<2> &R) const { sm2(S, 0, cs, R.b); }
     template <int V>
-    __device__ void compute(long long, const Regs<V> &R, const double (&n)[V], const double (&)[V],
+    __device__ void compute(long long k, const Regs<V> &R, const double (&n)[V], const double (&)[V],
                             double (&acc)[1][V]) const {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const double t = __dsub_rn(R.b[v], n[v]);
-            acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(t, t));
+            accp(acc, 0, v, sk, k, __dmul_rn(t, t));
         }
     }
 };
@@ -199,6 +202,7 @@ struct BodyTrue {
 struct BodyInitW {
     static constexpr int NQ = 3;
     static constexpr bool kStencil = true;
+    Sink sk;              // reference-order product sink
     const double *r, *u;
     double *w;
     double sigma;
@@ -207,7 +211,7 @@ struct BodyInitW {
     double *mout;
     template <int V> struct Regs { double r[V], u[V], d[V]; };
     static constexpr int kTmaStreams = 1;                 // r (identity preconditioner: u == r)
-    __device__ void setup(const Ws &) {}
+    __device__ void setup(const Ws &ws) { sk.set(ws); }
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
         ld_cs<V>(r, k, R.r);
         if (!ident) ld_cs<V>(u, k, R.u);
@@ -223,9 +227,9 @@ struct BodyInitW {
             const double uu = uc[v];
             ww[v] = axpy1(-sigma, R.r[v], n[v]);
             const double dv = axpy1(sigma, R.r[v], ww[v]);
-            acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(R.r[v], uu));
-            acc[1][v] = __dadd_rn(acc[1][v], __dmul_rn(dv, uu));
-            acc[2][v] = __dadd_rn(acc[2][v], __dmul_rn(R.r[v], R.r[v]));
+            accp(acc, 0, v, sk, k, __dmul_rn(R.r[v], uu));
+            accp(acc, 1, v, sk, k, __dmul_rn(dv, uu));
+            accp(acc, 2, v, sk, k, __dmul_rn(R.r[v], R.r[v]));
         }
         st_cs<V>(w, k, ww);
         if (mout) {
@@ -252,6 +256,7 @@ template <int PC, bool VAR = false>
 struct BodyPcgIter {
     static constexpr int NQ = 4;
     static constexpr bool kStencil = true;
+    Sink sk;              // reference-order product sink
     double *x, *r, *u, *z, *q, *s, *t, *p;
     double *w0, *w1;
     const double *dinv;
@@ -270,6 +275,7 @@ struct BodyPcgIter {
         if constexpr (PC != KPL_PC_IDENTITY) { sm2(S, 5, cs, R.u); sm2(S, 6, cs, R.q); sm2(S, 7, cs, R.p); }
     }
     __device__ void setup(const Ws &ws) {
+        sk.set(ws);
         alpha = __ldcg(&ws.head->alpha);
         beta = __ldcg(&ws.head->beta);
         if constexpr (VAR) {
@@ -333,10 +339,10 @@ struct BodyPcgIter {
             else uo[v] = sub2(uin, alpha, qn, asig, pn);        // u = _sub2(u, a, q, asig, p)
             if constexpr (!VAR) wo[v] = __dsub_rn(w, __dmul_rn(alpha, zo[v]));   // w = w - alpha*z
             const double dv = axpy1(sigma, ro[v], wo[v]);       // axpy(sigma, r, w)
-            acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(ro[v], uo[v]));
-            acc[1][v] = __dadd_rn(acc[1][v], __dmul_rn(dv, uo[v]));
-            acc[2][v] = __dadd_rn(acc[2][v], __dmul_rn(ro[v], ro[v]));
-            if (want_xi) acc[3][v] = __dadd_rn(acc[3][v], __dmul_rn(xo[v], xo[v]));
+            accp(acc, 0, v, sk, k, __dmul_rn(ro[v], uo[v]));
+            accp(acc, 1, v, sk, k, __dmul_rn(dv, uo[v]));
+            accp(acc, 2, v, sk, k, __dmul_rn(ro[v], ro[v]));
+            if (want_xi) accp(acc, 3, v, sk, k, __dmul_rn(xo[v], xo[v]));
         }
         st_cs<V>(x, k, xo);
         st_cs<V>(r, k, ro);
@@ -372,12 +378,14 @@ template <int MODE>
 struct BodyGap {
     static constexpr int NQ = MODE == GAP_F ? 2 : 1;
     static constexpr bool kStencil = true;
+    Sink sk;              // reference-order product sink
     const double *b, *r, *t, *s, *z, *w0, *w1;
     const double *schedule;
     double sig;
     const double *w;
     template <int V> struct Regs { double a[V], c[V]; };
     __device__ void setup(const Ws &ws) {
+        sk.set(ws);
         w = pick(ws.head, SEL_ITER, w0, w1);
         if (schedule) sig = schedule[ws.head->iter];
     }
@@ -388,20 +396,20 @@ struct BodyGap {
         if constexpr (MODE == GAP_J) { ld_cs<V>(z, k, R.c); }
     }
     template <int V>
-    __device__ void compute(long long, const Regs<V> &R, const double (&n)[V], const double (&)[V],
+    __device__ void compute(long long k, const Regs<V> &R, const double (&n)[V], const double (&)[V],
                             double (&acc)[NQ][V]) const {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             if constexpr (MODE == GAP_F) {
                 const double tr = __dsub_rn(R.a[v], n[v]);
                 const double f = __dsub_rn(tr, R.c[v]);
-                acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(tr, tr));
-                acc[1][v] = __dadd_rn(acc[1][v], __dmul_rn(f, f));
+                accp(acc, 0, v, sk, k, __dmul_rn(tr, tr));
+                accp(acc, 1, v, sk, k, __dmul_rn(f, f));
             } else {
                 double g;
                 if constexpr (MODE == GAP_J) g = __dsub_rn(n[v], R.c[v]);
                 else g = __dsub_rn(axpy1(-sig, R.a[v], n[v]), R.c[v]);
-                acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(g, g));
+                accp(acc, 0, v, sk, k, __dmul_rn(g, g));
             }
         }
     }
@@ -412,10 +420,12 @@ struct BodyGap {
 struct BodyCgP {
     static constexpr int NQ = 1;
     static constexpr bool kStencil = true;
+    Sink sk;              // reference-order product sink
     double *p0, *p1, *s;
     double *pout;
     template <int V> struct Regs { double d; };
     __device__ void setup(const Ws &ws) {
+        sk.set(ws);
         pout = const_cast<double *>(pick(ws.head, SEL_ITER1, p0, p1));
     }
     template <int V> __device__ void load(long long, Regs<V> &) const {}
@@ -423,7 +433,7 @@ struct BodyCgP {
     __device__ void compute(long long k, const Regs<V> &, const double (&n)[V], const double (&pn)[V],
                             double (&acc)[1][V]) const {
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(n[v], pn[v]));
+        for (int v = 0; v < V; ++v) accp(acc, 0, v, sk, k, __dmul_rn(n[v], pn[v]));
         st_cs<V>(pout, k, pn);
         st_cs<V>(s, k, n);
     }
@@ -435,12 +445,14 @@ template <int PC>
 struct BodyCgX {
     static constexpr int NQ = 2;
     static constexpr bool kStencil = false;
+    Sink sk;              // reference-order product sink
     double *x, *r, *u, *p0, *p1;
     const double *s, *dinv;
     double c, alpha;
     const double *p;
     template <int V> struct Regs { double x[V], r[V], s[V], p[V], d[V]; };
     __device__ void setup(const Ws &ws) {
+        sk.set(ws);
         alpha = ws.head->cg_alpha;
         p = pick(ws.head, SEL_ITER1, p0, p1);
     }
@@ -462,8 +474,8 @@ struct BodyCgX {
             if constexpr (PC == KPL_PC_IDENTITY) uo[v] = ro[v];
             else if constexpr (PC == KPL_PC_JACOBI_CONST) uo[v] = __dmul_rn(ro[v], c);
             else uo[v] = __dmul_rn(ro[v], R.d[v]);
-            acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(ro[v], uo[v]));
-            acc[1][v] = __dadd_rn(acc[1][v], __dmul_rn(ro[v], ro[v]));
+            accp(acc, 0, v, sk, k, __dmul_rn(ro[v], uo[v]));
+            accp(acc, 1, v, sk, k, __dmul_rn(ro[v], ro[v]));
         }
         st_cs<V>(x, k, xo);
         st_cs<V>(r, k, ro);
@@ -522,12 +534,13 @@ struct BodyRepl {
 struct BodyReplZ {
     static constexpr int NQ = 3;
     static constexpr bool kStencil = true;
+    Sink sk;              // reference-order product sink
     double *z;
     const double *r, *u, *w0, *w1;
     int ident;
     const double *w;
     template <int V> struct Regs { double r[V], u[V], w[V]; };
-    __device__ void setup(const Ws &ws) { w = pick(ws.head, SEL_ITER1, w0, w1); }
+    __device__ void setup(const Ws &ws) { sk.set(ws); w = pick(ws.head, SEL_ITER1, w0, w1); }
     template <int V> __device__ void load(long long k, Regs<V> &R) const {
         ld_cs<V>(r, k, R.r);
         ld_cs<V>(w, k, R.w);
@@ -539,9 +552,9 @@ struct BodyReplZ {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const double uu = ident ? R.r[v] : R.u[v];
-            acc[0][v] = __dadd_rn(acc[0][v], __dmul_rn(R.r[v], uu));
-            acc[1][v] = __dadd_rn(acc[1][v], __dmul_rn(R.w[v], uu));
-            acc[2][v] = __dadd_rn(acc[2][v], __dmul_rn(R.r[v], R.r[v]));
+            accp(acc, 0, v, sk, k, __dmul_rn(R.r[v], uu));
+            accp(acc, 1, v, sk, k, __dmul_rn(R.w[v], uu));
+            accp(acc, 2, v, sk, k, __dmul_rn(R.r[v], R.r[v]));
         }
         st_cs<V>(z, k, n);
     }

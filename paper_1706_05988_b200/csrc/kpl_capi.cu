@@ -46,6 +46,9 @@ constexpr int kSMs = 148;
 int make_layout(const kpl_op *op, Layout &L) {
     if (!op) return fail(KPL_EINVAL, "null operator");
     std::memset(&L, 0, sizeof(L));
+    if (op->order != KPL_ORDER_TREE && op->order != KPL_ORDER_BLOCKED8) return fail(KPL_EINVAL, "unknown order");
+    if (op->order == KPL_ORDER_BLOCKED8 && op->chunks_global > 0)
+        return fail(KPL_EUNSUPPORTED, "reference (blocked) order is single-GPU only");
     if (op->kind == KPL_OP_STENCIL) {
         if (op->nx < 1 || op->ny < 1 || op->nz < 1) return fail(KPL_EINVAL, "grid dimensions must be >= 1");
         if (op->n != op->nx * op->ny * op->nz) return fail(KPL_EINVAL, "n != nx*ny*nz");
@@ -85,7 +88,9 @@ int make_layout(const kpl_op *op, Layout &L) {
     return fail(KPL_EINVAL, "unknown operator kind");
 }
 
-struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, mbuf, total; };
+struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, mbuf, prod, total; };
+
+bool ordered(const kpl_op *op) { return op->order == KPL_ORDER_BLOCKED8; }
 
 // CSR with a vector Jacobi on one GPU keeps m = w * inv_diag next to w, so the
 // SpMV gathers one vector per nonzero instead of two (w and inv_diag).
@@ -103,7 +108,8 @@ Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     o.reps = o.hist + align256(8LL * HC * (max_iters + 1));
     o.nbuf = o.reps + align256(8LL * (max_iters + 1));
     o.mbuf = o.nbuf + (op->kind == KPL_OP_CSR && op->row_ptr ? align256(8LL * op->n) : 0);
-    o.total = o.mbuf + (use_mbuf(op) ? align256(8LL * op->n) : 0);
+    o.prod = o.mbuf + (use_mbuf(op) ? align256(8LL * op->n) : 0);
+    o.total = o.prod + (ordered(op) ? align256(8LL * NQ * op->n) : 0);
     return o;
 }
 
@@ -121,7 +127,9 @@ Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspa
     ws.mbuf = use_mbuf(op) ? reinterpret_cast<double *>(base + o.mbuf) : nullptr;
     ws.chunk_offset = op->chunks_global > 0 ? op->chunk_offset : 0;
     ws.chunks_global = op->chunks_global > 0 ? op->chunks_global : L.nch;
-    ws.inline_final = op->chunks_global > 0 ? 0 : 1;
+    ws.inline_final = op->chunks_global > 0 || ordered(op) ? 0 : 1;
+    ws.prod = ordered(op) ? reinterpret_cast<double *>(base + o.prod) : nullptr;
+    ws.nprod = op->n;
     return ws;
 }
 
@@ -171,6 +179,10 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
         }
         csr_chunk_sweep<In, Body><<<(unsigned)std::min(L.nch, cap), NT, 0, st>>>(g, L, in, body, ws.nbuf, ws, cfg,
                                                                                phase, pred, row);
+    }
+    if (ws.prod && phase != PH_NONE && Body::NQ > 0) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        blocked_final_kernel<<<1, 32, 0, st>>>(ws, cfg, phase, pred, row, Body::NQ);
     }
     return cuda_check("sweep launch");
 }
@@ -260,7 +272,7 @@ bool encode_box(CUtensorMap *m, const double *base, const kpl_op *op, unsigned b
 bool tma_eligible(const kpl_op *op, const Layout &L) {
     const bool shape3d = L.wx == 1 && L.wy == NWARP;             // 64 x 8 tiles
     const bool shape2d = L.wx == NWARP && L.wy == 1 && op->ny == 1;  // 512 x 1 tiles (2D grids)
-    return op->kind == KPL_OP_STENCIL && op->precond != KPL_PC_JACOBI_VEC && L.vx == 2 &&
+    return op->kind == KPL_OP_STENCIL && op->precond != KPL_PC_JACOBI_VEC && L.vx == 2 && !ordered(op) &&
            (shape3d || shape2d) && !op->halo_lo && !op->halo_hi && op->nx % 2 == 0 && tma_available();
     // (op->zhalo is supported: the stencil-input maps then cover planes -1..nz)
 }
@@ -776,7 +788,7 @@ int kpl_solver_iterate_persistent(const kpl_op *op, const kpl_cfg *cfgp, const k
     int rc = make_ctx(op, cfgp, v, workspace, stream, c);
     if (rc != KPL_OK) return rc;
     const int m = c.cfg.method;
-    if (op->kind != KPL_OP_STENCIL || op->chunks_global > 0 || c.cfg.track_gaps ||
+    if (op->kind != KPL_OP_STENCIL || op->chunks_global > 0 || ordered(op) || c.cfg.track_gaps ||
         !(m == KPL_M_PCG || m == KPL_M_PCG_SH || m == KPL_M_PCG_VAR_SH))
         return fail(KPL_EUNSUPPORTED, "persistent solve: single-GPU stencil p-CG / p-CG-sh / var-sh only");
     if (count <= 0) return KPL_OK;

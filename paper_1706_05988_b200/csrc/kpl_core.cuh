@@ -78,7 +78,24 @@ struct Ws {                   // device view of the caller's workspace
     long long chunk_offset;   // first global chunk of this rank
     long long chunks_global;
     int inline_final;         // 1: last CTA finalises (single GPU)
+    double *prod;             // KPL_ORDER_BLOCKED8: products [NQ][nprod] for blocked_final_kernel
+    long long nprod;
 };
+
+// Product sink of the reference-order mode: bodies accumulate through accp(),
+// which also stores each product when the workspace carries a product buffer.
+struct Sink {
+    double *p = nullptr;
+    long long n = 0;
+    __device__ __forceinline__ void set(const Ws &ws) { p = ws.prod; n = ws.nprod; }
+};
+
+template <int Q, int V>
+__device__ __forceinline__ void accp(double (&acc)[Q][V], int q, int v, const Sink &sk, long long k,
+                                     double prod) {
+    acc[q][v] = __dadd_rn(acc[q][v], prod);
+    if (sk.p) sk.p[q * sk.n + k + v] = prod;
+}
 
 struct Cfg {                  // scalar view of kpl_cfg
     int method;

@@ -434,4 +434,50 @@ __global__ void __launch_bounds__(NT) finalize_kernel(Ws ws, Cfg cfg, int phase,
     if (threadIdx.x == 0) finalize(ws, cfg, phase, f);
 }
 
+// Reference-order fold (KPL_ORDER_BLOCKED8): one warp, thread (q, lane) runs
+// lane `lane` of _kernels.py:16-41 over products prod[q][lane + 8j] -- the
+// same sequential chain a0 += u[k]*v[k] -- then the pairwise lane fold and
+// the tail, and the epilogue of `phase` on the result.  The products were
+// stored by the sweep that just ran (accp), so the values are bit-identical
+// to the reference's blocked_dot of the same vectors.
+__global__ void __launch_bounds__(32) blocked_final_kernel(Ws ws, Cfg cfg, int phase, int pred, long long row,
+                                                           int nq) {
+    __shared__ double lanes[NQ][8];
+    __shared__ double tails[NQ];
+    if (!pred_ok(ws.head, pred, row)) return;
+    const int q = threadIdx.x >> 3, lane = threadIdx.x & 7;
+    const long long n = ws.nprod, lim = n - n % 8;
+    if (q < nq) {
+        const double *p = ws.prod + q * n + lane;
+        double a = 0.0;
+        long long k = 0;
+        constexpr int U = 16;
+        for (; k + 8LL * U <= lim; k += 8LL * U) {
+            double t[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) t[j] = __ldcg(p + k + 8LL * j);
+#pragma unroll
+            for (int j = 0; j < U; ++j) a = __dadd_rn(a, t[j]);
+        }
+        for (; k < lim; k += 8) a = __dadd_rn(a, __ldcg(p + k));
+        lanes[q][lane] = a;
+        if (lane == 0) {
+            double t = 0.0;
+            for (long long j = lim; j < n; ++j) t = __dadd_rn(t, __ldcg(ws.prod + q * n + j));
+            tails[q] = t;
+        }
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        double v[NQ] = {0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i < nq; ++i) {
+            const double *l = lanes[i];
+            v[i] = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(l[0], l[1]), __dadd_rn(l[2], l[3])),
+                                       __dadd_rn(__dadd_rn(l[4], l[5]), __dadd_rn(l[6], l[7]))),
+                             tails[i]);
+        }
+        finalize(ws, cfg, phase, v);
+    }
+}
+
 }  // namespace kpl

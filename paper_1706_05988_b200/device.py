@@ -13,6 +13,8 @@ only receives raw pointers.
 
 from __future__ import annotations
 
+import contextlib
+import os
 import weakref
 
 import numpy as np
@@ -21,6 +23,41 @@ from . import _lib
 from ._lib import KplError, KplOp
 
 _torch = None
+
+# Reduction order of dot products / norms (kpl_op.order):
+#   "tree"      fixed tile/chunk tree, bandwidth-bound (default)
+#   "reference" the reference's blocked_dot order (_kernels.py:16-41): device
+#               results are bit-identical to the reference's own solvers, at
+#               the cost of a sequential n/8-long fold after each reducing sweep
+ORDERS = {"tree": _lib.KPL_ORDER_TREE, "reference": _lib.KPL_ORDER_BLOCKED8}
+_order = os.environ.get("KPL_REDUCTION_ORDER", "tree")
+
+
+def _check_order(name):
+    if name not in ORDERS:
+        raise ValueError(f"unknown reduction order {name!r} (expected one of {sorted(ORDERS)})")
+    return name
+
+
+def get_reduction_order() -> str:
+    return _check_order(_order)
+
+
+def set_reduction_order(name: str) -> str:
+    """Set the process-wide reduction order; returns the previous one."""
+    global _order
+    prev, _order = _order, _check_order(name)
+    return prev
+
+
+@contextlib.contextmanager
+def reduction_order(name: str):
+    """`with reduction_order("reference"): solve(...)` -- scoped order."""
+    prev = set_reduction_order(name)
+    try:
+        yield
+    finally:
+        set_reduction_order(prev)
 
 
 def torch():
@@ -176,6 +213,7 @@ def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk
     op.zc = zc
     op.vx = vx
     op.chunk_blocks = chunk_blocks
+    op.order = ORDERS[get_reduction_order()]
     if dp is not None:
         op.pc_const = dp.const
         op.inv_diag = ptr(dp.inv_diag)
@@ -187,6 +225,7 @@ def vector_op(n) -> KplOp:
     op = KplOp()
     op.kind = _lib.KPL_OP_CSR
     op.n = n
+    op.order = ORDERS[get_reduction_order()]
     return op
 
 

@@ -555,6 +555,9 @@ def solve_distributed(A, M, b_local, x0_local, cfg: SolverConfig, comm=None, zc=
     `b_local` / `x0_local`: this rank's rows (plan.local_slice(rank)), or, with
     a LocalComm, a list with one block per rank.  Returns a SolveResult whose
     `x` is the list of local blocks and whose history is global."""
+    if D.get_reduction_order() != "tree":
+        raise _lib.KplError("the reference (blocked) reduction order is single-GPU only; "
+                            "partitioned solves use the P-invariant chunk tree")
     if comm is None:
         comm = TorchComm()
     S = DistributedSolve(A, M, cfg, comm, zc=zc, chunk_blocks=chunk_blocks)

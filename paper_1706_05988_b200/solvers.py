@@ -214,7 +214,8 @@ class _Solve:
         self.status = _lib.KplStatus()
         if persistent is None:
             persistent = (self.dm.kind == _lib.KPL_OP_STENCIL and n <= self.PERSISTENT_MAX_N
-                          and cfg.method in ("pcg", "pcg_sh", "pcg_var_sh") and not cfg.track_gaps)
+                          and cfg.method in ("pcg", "pcg_sh", "pcg_var_sh") and not cfg.track_gaps
+                          and self.op.order == _lib.KPL_ORDER_TREE)
         self.persistent = bool(persistent)
         # classic CG records row i in the first half of pass i, so the final
         # row max_iters needs one more pass than the pipelined solvers

@@ -36,6 +36,51 @@ def test_library_layout_queries_without_gpu():
     assert b"grid" in lib.kpl_last_error()
 
 
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """sizeof/offsetof of every ABI struct, compiled from include/kpl_b200.h
+    with gcc, equal the ctypes mirrors the Python host side passes."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    structs = {"kpl_op": _lib.KplOp, "kpl_cfg": _lib.KplCfg, "kpl_vecs": _lib.KplVecs,
+               "kpl_status": _lib.KplStatus}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "kpl_b200.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["return 0; }"]
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                   check=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, f"{cname}.{fname}"
+
+
+def test_reduction_order_field_validation():
+    lib = _lib.load()
+    op = _lib.KplOp()
+    op.kind, op.n = _lib.KPL_OP_CSR, 1000
+    tree = lib.kpl_workspace_bytes(op, 10)
+    op.order = _lib.KPL_ORDER_BLOCKED8
+    assert lib.kpl_workspace_bytes(op, 10) >= tree + 4 * 8 * 1000      # product buffer
+    op.chunks_global, op.chunk_offset = 8, 0
+    assert lib.kpl_workspace_bytes(op, 10) < 0                          # single GPU only
+    assert b"single-GPU" in lib.kpl_last_error()
+    op.chunks_global, op.order = 0, 2
+    assert lib.kpl_workspace_bytes(op, 10) == _lib.KPL_EINVAL
+    with K.reduction_order("reference"):
+        from paper_1706_05988_b200 import device
+        assert device.vector_op(5).order == _lib.KPL_ORDER_BLOCKED8
+    assert K.get_reduction_order() == "tree"
+
+
 def test_breakdown_messages_match_reference():
     lib = _lib.load()
     msgs = [lib.kpl_breakdown_message(i).decode() for i in range(1, 7)]
