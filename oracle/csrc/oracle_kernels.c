@@ -14,6 +14,7 @@
  */
 #include <stdint.h>
 #include <stddef.h>
+#include <math.h>
 
 /* pkg/src/kpl/_kernels.py:15-41  blocked_dot: 8 interleaved lanes over k mod 8,
  * fixed merge ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)), then + sequential tail. */
@@ -78,4 +79,66 @@ void orc_stencil_matvec(int64_t NX, int64_t NY, int64_t NZ, double diag,
                 if (z < NZ - 1) acc += -1.0 * v[id + sxy];
                 out[id] = acc;
             }
+}
+
+/* pkg/src/kpl/_kernels.py:55-63  lower_solve: forward substitution with a
+ * lower-triangular CSR factor whose diagonal is the last entry of each row;
+ * acc starts at b[i] and subtracts values[k]*out[col] in stored order, then
+ * one division by the diagonal. */
+void orc_lower_solve(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                     const double *values, const double *b, double *out)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t d = row_ptr[i + 1] - 1;
+        double acc = b[i];
+        for (int64_t k = row_ptr[i]; k < d; ++k)
+            acc -= values[k] * out[col_idx[k]];
+        out[i] = acc / values[d];
+    }
+}
+
+/* pkg/src/kpl/_kernels.py:66-74  upper_solve: backward substitution with the
+ * transposed factor (diagonal first in each row), rows from n-1 down. */
+void orc_upper_solve(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                     const double *values, const double *b, double *out)
+{
+    for (int64_t i = n - 1; i >= 0; --i) {
+        const int64_t d = row_ptr[i];
+        double acc = b[i];
+        for (int64_t k = d + 1; k < row_ptr[i + 1]; ++k)
+            acc -= values[k] * out[col_idx[k]];
+        out[i] = acc / values[d];
+    }
+}
+
+/* pkg/src/kpl/_kernels.py:77-115  ic0_factor: row-by-row IC(0) on the
+ * lower pattern (sorted columns, diagonal last).  Off-diagonal (i, c):
+ * s = a - sum over the shared strictly-lower columns (merge walk, ascending)
+ * of l[i,*] * l[c,*], then s / l[c,c]; the pivot is a[i,i] - sum l[i,k]^2 in
+ * row order, square-rooted.  Returns -1, or the first row with pivot <= 0. */
+int64_t orc_ic0_factor(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                       const double *a_values, double *l_values)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t lo = row_ptr[i], di = row_ptr[i + 1] - 1;
+        for (int64_t kk = lo; kk < di; ++kk) {
+            const int64_t c = col_idx[kk];
+            const int64_t dc = row_ptr[c + 1] - 1;
+            double s = a_values[kk];
+            int64_t p = lo, q = row_ptr[c];
+            while (p < kk && q < dc) {
+                if (col_idx[p] == col_idx[q]) { s -= l_values[p] * l_values[q]; ++p; ++q; }
+                else if (col_idx[p] < col_idx[q]) ++p;
+                else ++q;
+            }
+            l_values[kk] = s / l_values[dc];
+        }
+        double d = a_values[di];
+        for (int64_t kk = lo; kk < di; ++kk)
+            d -= l_values[kk] * l_values[kk];
+        if (d <= 0.0)
+            return i;
+        l_values[di] = sqrt(d);
+    }
+    return -1;
 }

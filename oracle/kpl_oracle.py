@@ -21,6 +21,8 @@ What it restates (file:line into the read-only reference `pkg/src/kpl/`):
 * `solve_pcg_var_shifted` -> `solvers.py:425-498`
 * `_ReplacementTrigger` / `solve_pcg_rr` -> `solvers.py:501-608`
 * Jacobi apply       -> `precond.py:82-94` (`v * inv_diag`; identity returns v)
+* IC(0)              -> `precond.py:28-53, :134-154`, `_kernels.py:55-115` (C: lower/upper
+                        solves and the factor)
 * `laplacian_2d`     -> `sparse.py:188-214`; `random_spd` -> `sparse.py:217-228`
 * `from_coo`         -> `sparse.py:89-110`
 
@@ -74,6 +76,11 @@ def _clib():
         lib.orc_csr_matvec.argtypes = [i64, p, p, p, p, p]
         lib.orc_stencil_matvec.restype = None
         lib.orc_stencil_matvec.argtypes = [i64, i64, i64, d, p, p]
+        for name in ("orc_lower_solve", "orc_upper_solve"):
+            getattr(lib, name).restype = None
+            getattr(lib, name).argtypes = [i64, p, p, p, p, p]
+        lib.orc_ic0_factor.restype = i64
+        lib.orc_ic0_factor.argtypes = [i64, p, p, p, p]
         _lib = lib
     return _lib
 
@@ -219,16 +226,75 @@ def axpy(alpha, x, y):
 
 
 class Precond:
-    """precond.py:56-131 restricted to identity / Jacobi."""
+    """precond.py:56-131: identity, Jacobi, IC(0) (`lower` = (row_ptr,
+    col_idx, l_values) of L, `upper` = the same for L^T)."""
 
-    def __init__(self, kind="identity", inv_diag=None):
+    def __init__(self, kind="identity", inv_diag=None, lower=None, upper=None):
         self.kind = kind
         self.inv_diag = inv_diag
+        self.lower = lower
+        self.upper = upper
 
     def apply(self, v):
         if self.kind == "identity":
             return v                                     # precond.py:84-85
-        return v * self.inv_diag                         # precond.py:88-89
+        if self.kind == "jacobi":
+            return v * self.inv_diag                     # precond.py:88-89
+        v = np.ascontiguousarray(v, dtype=np.float64)   # precond.py:90-94
+        n = len(v)
+        y, out = np.empty(n), np.empty(n)
+        lib = _clib()
+        lib.orc_lower_solve(n, *(_ptr(a) for a in self.lower), _ptr(v), _ptr(y))
+        lib.orc_upper_solve(n, *(_ptr(a) for a in self.upper), _ptr(y), _ptr(out))
+        return out
+
+
+class PreconditionerBreakdown(ArithmeticError):
+    """precond.py:20-25."""
+
+    def __init__(self, row):
+        self.row = row
+        super().__init__(f"nonpositive pivot in IC(0) factorization at row {row}")
+
+
+def lower_pattern(A, eta=0.0):
+    """precond.py:28-43: lower triangle of A (diagonal last per row), the
+    diagonal scaled by (1 + eta) when eta != 0."""
+    n = A.n
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(A.row_ptr))
+    keep = A.col_idx <= rows
+    cols = np.ascontiguousarray(A.col_idx[keep], dtype=np.int64)
+    vals = np.array(A.values[keep], dtype=np.float64)
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum(np.bincount(rows[keep], minlength=n))
+    dpos = ptr[1:] - 1
+    if np.any(ptr[1:] == ptr[:-1]) or np.any(cols[dpos] != np.arange(n)):
+        raise ValueError("matrix has a structurally missing diagonal entry")
+    if eta:
+        vals[dpos] *= 1.0 + eta
+    return ptr, cols, vals
+
+
+def transpose_pattern(n, ptr, cols, vals):
+    """precond.py:46-53: CSR of the transpose, rows of each column in order."""
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr))
+    perm = np.lexsort((rows, cols))
+    tptr = np.zeros(n + 1, dtype=np.int64)
+    tptr[1:] = np.cumsum(np.bincount(cols, minlength=n))
+    return tptr, np.ascontiguousarray(rows[perm]), np.ascontiguousarray(vals[perm])
+
+
+def make_ic0(A, eta=0.0):
+    """precond.py:134-154 with the factor of _kernels.py:77-115 (C)."""
+    if eta < 0.0:
+        raise ValueError("compensation shift eta must be >= 0")
+    ptr, cols, avals = lower_pattern(A, eta)
+    lvals = np.zeros_like(avals)
+    bad = int(_clib().orc_ic0_factor(A.n, _ptr(ptr), _ptr(cols), _ptr(avals), _ptr(lvals)))
+    if bad >= 0:
+        raise PreconditionerBreakdown(bad)
+    lower = (ptr, cols, lvals)
+    return Precond("ic0", lower=lower, upper=transpose_pattern(A.n, *lower))
 
 
 def identity():
@@ -256,7 +322,11 @@ def as_oracle_precond(M):
         if hasattr(inv, "cpu"):
             inv = inv.cpu().numpy()
         return Precond("jacobi", np.asarray(inv, dtype=np.float64))
-    raise ValueError(f"oracle supports identity/jacobi, not {kind!r}")
+    if kind == "ic0":
+        lower = tuple(np.ascontiguousarray(a, dtype=t) for a, t in
+                      zip(M.host_lower(), (np.int64, np.int64, np.float64)))
+        return Precond("ic0", lower=lower, upper=transpose_pattern(len(lower[0]) - 1, *lower))
+    raise ValueError(f"oracle supports identity/jacobi/ic0, not {kind!r}")
 
 
 # --------------------------------------------------------------------------

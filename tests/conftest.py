@@ -40,6 +40,11 @@ def gold_j3d():
     return golden("jacobi_3d")
 
 
+@pytest.fixture(scope="session")
+def gold_ic0():
+    return golden("ic0")
+
+
 def hist_equal(a, b):
     """Bitwise equality of two history arrays (NaN == NaN)."""
     a = np.asarray(a, dtype=np.float64)

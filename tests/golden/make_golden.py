@@ -250,10 +250,63 @@ def formats():
     np.savez_compressed(os.path.join(HERE, "formats.npz"), **out)
 
 
+def ic0():
+    """IC(0) factor, apply and solves (precond.py:134-154, _kernels.py:55-115)."""
+    from kpl import PreconditionerBreakdown, make_ic0
+    out = {}
+    rng = np.random.default_rng(77)
+    cases = (("lap12x9", laplacian_2d(12, 9), 0.0),
+             ("rspd40", random_spd(40, cond=1e3, seed=5), 0.0),
+             ("rspd40e", random_spd(40, cond=1e3, seed=5), 0.25),
+             ("vc5", SparseMatrix(*_csr_args(problems.varcoef_3d(5, seed=2))), 0.0),
+             ("band3k", SparseMatrix(*_csr_args(problems.banded_spd(3000, seed=4, band=100))), 0.1))
+    for tag, A, eta in cases:
+        M = make_ic0(A, eta=eta)
+        out.update(csr_arrays(A, tag))
+        out[f"{tag}_eta"] = np.float64(eta)
+        out[f"{tag}_L_row_ptr"], out[f"{tag}_L_col_idx"], out[f"{tag}_L_values"] = M._l
+        out[f"{tag}_mu_tilde"] = np.int64(M.mu_tilde)
+        v = rng.normal(size=A.n)
+        v[::11] = -0.0
+        out[f"{tag}_v"] = v
+        out[f"{tag}_Mv"] = M.apply(v)
+    try:
+        make_ic0(SparseMatrix.from_dense(np.array([[1.0, 2.0], [2.0, 1.0]])), eta=0.0)
+    except PreconditionerBreakdown as exc:
+        out["indef_row"] = np.int64(exc.row)
+    # solves: 2D Laplacian 30x20 and var-coef 6^3, IC(0) eta 0
+    A = laplacian_2d(30, 20)
+    M = make_ic0(A, eta=0.0)
+    b = spmv(A, np.full(A.n, 1.0 / np.sqrt(A.n)))
+    out["l2_b"] = b
+    sched = tuple(0.05 * (k % 7) for k in range(82))
+    for m, extra in (("cg", {}), ("pcg", {}), ("pcg_sh", {"shift": 0.5}),
+                     ("pcg_var_sh", {"shift_schedule": sched}), ("pcg_rr", {}),
+                     ("pcg_rrx", {"rtol": 0.0})):
+        for gaps in (False, True):
+            meth = "pcg_rr" if m == "pcg_rrx" else m      # rrx: past convergence, replacements fire
+            kw = {"rtol": 1e-10, **extra}
+            run_case(out, f"l2_{m}_{'g' if gaps else 'n'}", A, M, b,
+                     SolverConfig(method=meth, max_iters=80, track_gaps=gaps, **kw), keep_x=True)
+    A = SparseMatrix(*_csr_args(problems.varcoef_3d(6, seed=0)))
+    M = make_ic0(A, eta=0.0)
+    b = spmv(A, np.random.default_rng(3).standard_normal(A.n))
+    out["v6_b"] = b
+    for m, extra in (("cg", {}), ("pcg_sh", {"shift": 0.3}), ("pcg_rr", {})):
+        run_case(out, f"v6_{m}", A, M, b, SolverConfig(method=m, max_iters=300, rtol=1e-12, **extra),
+                 keep_x=True)
+    np.savez_compressed(os.path.join(HERE, "ic0.npz"), **out)
+
+
+def _csr_args(A):
+    return A.n, A.row_ptr, A.col_idx, A.values
+
+
 if __name__ == "__main__":
     print("reference kpl", kpl.__version__, "from", kpl.__file__)
     only = sys.argv[1:]
     for name, fn in (("kernels", kernels), ("solvers_small", solvers_small), ("config1", config1),
-                     ("jacobi_3d", jacobi_and_3d), ("shift", shift_selection), ("formats", formats)):
+                     ("jacobi_3d", jacobi_and_3d), ("shift", shift_selection), ("formats", formats),
+                     ("ic0", ic0)):
         if not only or name in only:
             fn()
