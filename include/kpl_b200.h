@@ -43,6 +43,7 @@ extern "C" {
 #define KPL_PC_IDENTITY     0   /* precond.py:84-85  apply returns v              */
 #define KPL_PC_JACOBI_CONST 1   /* precond.py:88-89  v * inv_diag, inv_diag == c  */
 #define KPL_PC_JACOBI_VEC   2   /* precond.py:88-89  v * inv_diag[k]              */
+#define KPL_PC_IC0          3   /* precond.py:90-94  L^-T L^-1 v (CSR, 1 GPU)     */
 
 typedef struct kpl_op {
     int32_t kind;            /* KPL_OP_*                                         */
@@ -83,6 +84,15 @@ typedef struct kpl_op {
                           of a sequential n/8-long fold after each sweep      */
     int32_t order;
     int32_t _reserved;
+    /* KPL_PC_IC0: the factor L (lower CSR, diagonal last in each row) and its
+       transpose U = L^T (diagonal first), as built by make_ic0
+       (precond.py:134-154, factor from kpl_ic0_factor)                      */
+    const int32_t *ic_l_row_ptr;
+    const int32_t *ic_l_col_idx;
+    const double  *ic_l_values;
+    const int32_t *ic_u_row_ptr;
+    const int32_t *ic_u_col_idx;
+    const double  *ic_u_values;
 } kpl_op;
 
 #define KPL_ORDER_TREE      0
@@ -223,6 +233,24 @@ int kpl_sweep(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, int32_t k
               void *workspace, void *stream);
 /* Reduction phase of a sweep kind (0 = no reduction / nothing to finalize). */
 int kpl_sweep_phase(int32_t kind);
+
+/* ---- IC(0) preconditioner (reference: precond.py:134-154, _kernels.py:55-115)
+   The factor and both substitutions run as sync-free row sweeps on the
+   device, bit-identical to the reference's sequential loops.              */
+/* Scratch bytes kpl_ic0_factor needs for an n-row factor.                  */
+int64_t kpl_ic0_scratch_bytes(int64_t n);
+/* l_values = IC(0) factor of the lower pattern (row_ptr, col_idx; diagonal
+   last) whose values are a_values (A's lower triangle); each diagonal entry
+   is multiplied by diag_scale = 1 + eta first (precond.py:41-42; x * 1.0 is
+   exact, so eta = 0 needs no special case).  *bad_row (host) = -1, or the
+   first row whose pivot is not positive (_kernels.py:112-113 ->
+   PreconditionerBreakdown).  Blocks until the factor is done.              */
+int kpl_ic0_factor(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const double *a_values,
+                   double diag_scale, double *l_values, void *scratch, int64_t *bad_row, void *stream);
+/* out = M^-1 v for the operator's preconditioner (identity: copy; Jacobi:
+   v * inv_diag; IC(0): upper_solve(lower_solve(v))) -- precond.py:82-94.
+   `workspace`: kpl_workspace_bytes(op, 0) bytes.                           */
+int kpl_precond_apply(const kpl_op *op, const double *v, double *out, void *workspace, void *stream);
 
 /* ---- multi-GPU hooks (one process per GPU; host drives NCCL) ----------- */
 /* dst[k] = src[idx[k]] for k < n: packs the rows a neighbour needs (the

@@ -18,7 +18,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "kpl_b200.h")
 # constants mirrored from include/kpl_b200.h
 KPL_OK, KPL_EINVAL, KPL_ECUDA, KPL_EUNSUPPORTED = 0, -1, -2, -3
 KPL_OP_STENCIL, KPL_OP_CSR = 1, 2
-KPL_PC_IDENTITY, KPL_PC_JACOBI_CONST, KPL_PC_JACOBI_VEC = 0, 1, 2
+KPL_PC_IDENTITY, KPL_PC_JACOBI_CONST, KPL_PC_JACOBI_VEC, KPL_PC_IC0 = 0, 1, 2, 3
 KPL_M_CG, KPL_M_PCG, KPL_M_PCG_SH, KPL_M_PCG_VAR_SH, KPL_M_PCG_RR = 0, 1, 2, 3, 4
 KPL_ST_RUNNING, KPL_ST_DONE, KPL_ST_BREAKDOWN = 0, 1, 2
 KPL_HIST_COLS = 10
@@ -39,7 +39,9 @@ class KplOp(ctypes.Structure):
                 ("zc", _i32), ("vx", _i32), ("halo_lo", _p), ("halo_hi", _p),
                 ("row_ptr", _p), ("col_idx", _p), ("values", _p), ("nnz", _i64),
                 ("chunk_blocks", _i32), ("zhalo", _i32), ("pc_const", _d), ("inv_diag", _p),
-                ("chunk_offset", _i64), ("chunks_global", _i64), ("order", _i32), ("_reserved", _i32)]
+                ("chunk_offset", _i64), ("chunks_global", _i64), ("order", _i32), ("_reserved", _i32),
+                ("ic_l_row_ptr", _p), ("ic_l_col_idx", _p), ("ic_l_values", _p),
+                ("ic_u_row_ptr", _p), ("ic_u_col_idx", _p), ("ic_u_values", _p)]
 
 
 class KplCfg(ctypes.Structure):
@@ -87,6 +89,9 @@ _SIGS = {
     "kpl_sweep": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), ctypes.POINTER(KplVecs),
                          _i32, _i64, _p, _p]),
     "kpl_sweep_phase": (_i32, [_i32]),
+    "kpl_ic0_scratch_bytes": (_i64, [_i64]),
+    "kpl_ic0_factor": (_i32, [_i64, _p, _p, _p, _d, _p, _p, ctypes.POINTER(_i64), _p]),
+    "kpl_precond_apply": (_i32, [ctypes.POINTER(KplOp), _p, _p, _p, _p]),
     "kpl_chunk_table": (_i32, [ctypes.POINTER(KplOp), _p, ctypes.POINTER(_p), ctypes.POINTER(_p),
                                ctypes.POINTER(_i64)]),
 }

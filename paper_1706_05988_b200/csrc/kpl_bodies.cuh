@@ -164,13 +164,14 @@ struct BodyInitR {
             rr[v] = __dsub_rn(R.b[v], n[v]);
             if constexpr (PC == KPL_PC_IDENTITY) uu[v] = rr[v];
             else if constexpr (PC == KPL_PC_JACOBI_CONST) uu[v] = __dmul_rn(rr[v], c);
-            else uu[v] = __dmul_rn(rr[v], R.d[v]);
+            else if constexpr (PC == KPL_PC_JACOBI_VEC) uu[v] = __dmul_rn(rr[v], R.d[v]);
+            else uu[v] = 0.0;                 // IC(0): u = M r by the substitution sweeps after
             accp(acc, 0, v, sk, k, __dmul_rn(xin[v], xin[v]));
             accp(acc, 1, v, sk, k, __dmul_rn(rr[v], rr[v]));
             accp(acc, 2, v, sk, k, __dmul_rn(rr[v], uu[v]));
         }
         st_cs<V>(r, k, rr);
-        if constexpr (PC != KPL_PC_IDENTITY) st_cs<V>(u, k, uu);
+        if constexpr (PC != KPL_PC_IDENTITY && PC != KPL_PC_IC0) st_cs<V>(u, k, uu);
         if (copy_x) st_cs<V>(x, k, xin);
     }
 };
@@ -267,6 +268,7 @@ struct BodyPcgIter {
     const double *schedule;
     double dsig;
     double *mout;          // CSR + vector Jacobi: also store m = w * inv_diag (next SpMV input)
+    const double *mld;     // IC(0): m = M^-1 w, materialised by the substitution sweeps
     template <int V> struct Regs { double x[V], r[V], z[V], s[V], t[V], u[V], q[V], p[V], d[V]; };
     // x, r, z, s, t (+ u, q, p with a constant-diagonal Jacobi)
     static constexpr int kTmaStreams = PC == KPL_PC_IDENTITY ? 5 : 8;
@@ -299,6 +301,7 @@ struct BodyPcgIter {
             ld_cs<V>(p, k, R.p);
         }
         if constexpr (PC == KPL_PC_JACOBI_VEC) ld_cs<V>(dinv, k, R.d);
+        if constexpr (PC == KPL_PC_IC0) ld_cs<V>(mld, k, R.d);
     }
     template <int V>
     __device__ void compute(long long k, const Regs<V> &R, const double (&n)[V], const double (&wc)[V],
@@ -310,7 +313,8 @@ struct BodyPcgIter {
             double m;
             if constexpr (PC == KPL_PC_IDENTITY) m = w;
             else if constexpr (PC == KPL_PC_JACOBI_CONST) m = __dmul_rn(w, c);
-            else m = __dmul_rn(w, R.d[v]);
+            else if constexpr (PC == KPL_PC_JACOBI_VEC) m = __dmul_rn(w, R.d[v]);
+            else m = R.d[v];                                   // IC(0): loaded m
             const double uin = (PC == KPL_PC_IDENTITY) ? R.r[v] : R.u[v];
             double qn, pn;
             if constexpr (!VAR) {
@@ -473,13 +477,14 @@ struct BodyCgX {
             ro[v] = __dsub_rn(R.r[v], __dmul_rn(alpha, R.s[v]));
             if constexpr (PC == KPL_PC_IDENTITY) uo[v] = ro[v];
             else if constexpr (PC == KPL_PC_JACOBI_CONST) uo[v] = __dmul_rn(ro[v], c);
-            else uo[v] = __dmul_rn(ro[v], R.d[v]);
+            else if constexpr (PC == KPL_PC_JACOBI_VEC) uo[v] = __dmul_rn(ro[v], R.d[v]);
+            else uo[v] = 0.0;                 // IC(0): u after the substitution sweeps
             accp(acc, 0, v, sk, k, __dmul_rn(ro[v], uo[v]));
             accp(acc, 1, v, sk, k, __dmul_rn(ro[v], ro[v]));
         }
         st_cs<V>(x, k, xo);
         st_cs<V>(r, k, ro);
-        if constexpr (PC != KPL_PC_IDENTITY) st_cs<V>(u, k, uo);
+        if constexpr (PC != KPL_PC_IDENTITY && PC != KPL_PC_IC0) st_cs<V>(u, k, uo);
     }
 };
 
@@ -517,7 +522,7 @@ struct BodyRepl {
             return;
         }
         st_cs<V>(s, k, n);
-        if constexpr (PC != KPL_PC_IDENTITY) {
+        if constexpr (PC != KPL_PC_IDENTITY && PC != KPL_PC_IC0) {
             double qq[V];
 #pragma unroll
             for (int v = 0; v < V; ++v) {
@@ -557,6 +562,32 @@ struct BodyReplZ {
             accp(acc, 2, v, sk, k, __dmul_rn(R.r[v], R.r[v]));
         }
         st_cs<V>(z, k, n);
+    }
+};
+
+// Products of vector pairs: acc[q] += a[q][k] * b[q][k].  IC(0) runs the
+// reductions that the fused bodies cannot (u = M r is produced by the
+// substitution sweeps after them) as this separate pass, with the same
+// per-element products, so the reduction tree and values are unchanged.
+template <int Q>
+struct BodyPairs {
+    static constexpr int NQ = Q;
+    static constexpr bool kStencil = false;
+    Sink sk;
+    const double *a[Q], *b[Q];
+    template <int V> struct Regs { double a[Q][V], b[Q][V]; };
+    __device__ void setup(const Ws &ws) { sk.set(ws); }
+    template <int V> __device__ void load(long long k, Regs<V> &R) const {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) { ld_cs<V>(a[q], k, R.a[q]); ld_cs<V>(b[q], k, R.b[q]); }
+    }
+    template <int V>
+    __device__ void compute(long long k, const Regs<V> &R, const double (&)[V], const double (&)[V],
+                            double (&acc)[NQ][V]) const {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) accp(acc, q, v, sk, k, __dmul_rn(R.a[q][v], R.b[q][v]));
     }
 };
 

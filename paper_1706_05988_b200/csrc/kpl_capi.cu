@@ -19,6 +19,7 @@
 #include "kpl_bodies.cuh"
 #include "kpl_sweep.cuh"
 #include "kpl_tma.cuh"
+#include "kpl_ic0.cuh"
 
 using namespace kpl;
 
@@ -49,6 +50,8 @@ int make_layout(const kpl_op *op, Layout &L) {
     if (op->order != KPL_ORDER_TREE && op->order != KPL_ORDER_BLOCKED8) return fail(KPL_EINVAL, "unknown order");
     if (op->order == KPL_ORDER_BLOCKED8 && op->chunks_global > 0)
         return fail(KPL_EUNSUPPORTED, "reference (blocked) order is single-GPU only");
+    if (op->precond == KPL_PC_IC0 && (op->kind != KPL_OP_CSR || op->chunks_global > 0))
+        return fail(KPL_EUNSUPPORTED, "IC(0) runs with single-GPU CSR operators");
     if (op->kind == KPL_OP_STENCIL) {
         if (op->nx < 1 || op->ny < 1 || op->nz < 1) return fail(KPL_EINVAL, "grid dimensions must be >= 1");
         if (op->n != op->nx * op->ny * op->nz) return fail(KPL_EINVAL, "n != nx*ny*nz");
@@ -88,14 +91,17 @@ int make_layout(const kpl_op *op, Layout &L) {
     return fail(KPL_EINVAL, "unknown operator kind");
 }
 
-struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, mbuf, prod, total; };
+struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, mbuf, prod, ic0, total; };
+
+bool is_ic0(const kpl_op *op) { return op->precond == KPL_PC_IC0; }
 
 bool ordered(const kpl_op *op) { return op->order == KPL_ORDER_BLOCKED8; }
 
 // CSR with a vector Jacobi on one GPU keeps m = w * inv_diag next to w, so the
 // SpMV gathers one vector per nonzero instead of two (w and inv_diag).
 bool use_mbuf(const kpl_op *op) {
-    return op->kind == KPL_OP_CSR && op->row_ptr && op->precond == KPL_PC_JACOBI_VEC && op->chunks_global <= 0;
+    return op->kind == KPL_OP_CSR && op->row_ptr && op->chunks_global <= 0 &&
+           (op->precond == KPL_PC_JACOBI_VEC || op->precond == KPL_PC_IC0);
 }
 
 Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
@@ -109,7 +115,9 @@ Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     o.nbuf = o.reps + align256(8LL * (max_iters + 1));
     o.mbuf = o.nbuf + (op->kind == KPL_OP_CSR && op->row_ptr ? align256(8LL * op->n) : 0);
     o.prod = o.mbuf + (use_mbuf(op) ? align256(8LL * op->n) : 0);
-    o.total = o.prod + (ordered(op) ? align256(8LL * NQ * op->n) : 0);
+    o.ic0 = o.prod + (ordered(op) ? align256(8LL * NQ * op->n) : 0);
+    // IC(0): y = L^-1 v, forward / backward row flags, two tickets
+    o.total = o.ic0 + (is_ic0(op) ? align256(8LL * op->n) + 2 * align256(4LL * op->n) + 256 : 0);
     return o;
 }
 
@@ -131,6 +139,32 @@ Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspa
     ws.prod = ordered(op) ? reinterpret_cast<double *>(base + o.prod) : nullptr;
     ws.nprod = op->n;
     return ws;
+}
+
+Ic0Ws make_ic0_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspace) {
+    Ic0Ws s{};
+    if (!is_ic0(op)) return s;
+    const Offsets o = offsets(op, L, max_iters);
+    char *base = static_cast<char *>(workspace) + o.ic0;
+    s.y = reinterpret_cast<double *>(base);
+    s.fflag = reinterpret_cast<int *>(base + align256(8LL * op->n));
+    s.bflag = reinterpret_cast<int *>(base + align256(8LL * op->n) + align256(4LL * op->n));
+    s.tickets = reinterpret_cast<unsigned int *>(base + align256(8LL * op->n) + 2 * align256(4LL * op->n));
+    return s;
+}
+
+Tri ic0_lower(const kpl_op *op) { return Tri{op->ic_l_row_ptr, op->ic_l_col_idx, op->ic_l_values}; }
+Tri ic0_upper(const kpl_op *op) { return Tri{op->ic_u_row_ptr, op->ic_u_col_idx, op->ic_u_values}; }
+
+// out = U^-1 L^-1 pick(v0, v1): the two sync-free substitution sweeps
+int ic0_apply(const kpl_op *op, const Ic0Ws &s, const WsHead *head, const double *v0, const double *v1,
+              int sel, double *out, int pred, long long row, cudaStream_t st) {
+    if (!op->ic_l_row_ptr || !op->ic_u_row_ptr) return fail(KPL_EINVAL, "IC(0) factor arrays missing");
+    const unsigned grid = (unsigned)cdiv(op->n, NT);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    ic0_lower_kernel<<<grid, NT, 0, st>>>(op->n, ic0_lower(op), v0, v1, sel, s, head, pred, row);
+    ic0_upper_kernel<<<grid, NT, 0, st>>>(op->n, ic0_upper(op), out, s, head, pred, row);
+    return cuda_check("IC(0) apply");
 }
 
 Cfg make_cfg(const kpl_cfg *c) {
@@ -208,7 +242,8 @@ int with_pc(const kpl_op *op, F &&f) {
         if (!op->inv_diag) return fail(KPL_EINVAL, "Jacobi needs inv_diag");
         return f(std::integral_constant<int, KPL_PC_JACOBI_VEC>());
     }
-    return fail(KPL_EUNSUPPORTED, "CSR operators take identity or vector Jacobi");
+    if (op->precond == KPL_PC_IC0) return f(std::integral_constant<int, KPL_PC_IC0>());
+    return fail(KPL_EUNSUPPORTED, "CSR operators take identity, vector Jacobi or IC(0)");
 }
 
 // ------------------------------------------------------------ TMA path
@@ -336,6 +371,13 @@ __global__ void gather_kernel(long long n, const int *__restrict__ idx, const do
                               double *__restrict__ dst) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += gridDim.x * (long long)blockDim.x)
         dst[k] = __ldg(src + idx[k]);
+}
+
+// precond.py:88-89: v * inv_diag (one rounding); `d` NULL -> the constant c
+__global__ void jacobi_kernel(long long n, const double *__restrict__ d, double c, const double *__restrict__ v,
+                              double *__restrict__ out) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += gridDim.x * (long long)blockDim.x)
+        out[k] = __dmul_rn(v[k], d ? d[k] : c);
 }
 
 __global__ void axpy_kernel(long long n, double a, const double *__restrict__ x, const double *__restrict__ y,
@@ -484,6 +526,8 @@ struct Ctx {
     const kpl_vecs *v;
     cudaStream_t st;
     bool ident;
+    bool ic0;              // IC(0): M^-1 by the substitution sweeps between fused sweeps
+    Ic0Ws ic;
     double sigma;
 };
 
@@ -498,6 +542,9 @@ int make_ctx(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, void *wor
     c.v = v;
     c.st = (cudaStream_t)stream;
     c.ident = op->precond == KPL_PC_IDENTITY;
+    c.ic0 = is_ic0(op);
+    c.ic = make_ic0_ws(op, c.L, c.cfg.max_iters, workspace);
+    if (c.ic0 && (!op->ic_l_row_ptr || !op->ic_u_row_ptr)) return fail(KPL_EINVAL, "IC(0) factor arrays missing");
     // sigma of the fixed-shift recurrences; pcg_var_sh passes schedule[0] here
     // (used by the init sweep) and reads the rest of the schedule on the device
     c.sigma = (c.cfg.method == KPL_M_PCG_SH || c.cfg.method == KPL_M_PCG_VAR_SH) ? c.cfg.shift : 0.0;
@@ -546,31 +593,43 @@ int do_sweep(const Ctx &c, int kind, long long row) {
         return launch(op, L, InNone(), body, c.ws, c.cfg, phase, pred, row, c.st);
     }
     case KPL_SW_INIT_R:                  // r = b - A x; u = M r  (solvers.py:374-375)
-    case KPL_SW_RR_R:                    // replacement r = b - A x, u = M r (:600-601)
-        return with_pc(op, [&](auto pc) -> int {
+    case KPL_SW_RR_R: {                  // replacement r = b - A x, u = M r (:600-601)
+        const int ph = c.ic0 ? PH_NONE : phase;
+        rc = with_pc(op, [&](auto pc) -> int {
             constexpr int PC = decltype(pc)::value;
             BodyInitR<PC> body;
             body.b = v->b; body.x = v->x; body.r = v->r; body.u = v->u;
             body.dinv = op->inv_diag; body.c = op->pc_const; body.copy_x = 0;
-            if constexpr (PC != KPL_PC_JACOBI_VEC) {
+            if constexpr (PC != KPL_PC_JACOBI_VEC && PC != KPL_PC_IC0) {
                 if (tma) {
                     const double *streams[1] = {v->b};
-                    return launch_tma(op, L, v->x, v->x, 0, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
+                    return launch_tma(op, L, v->x, v->x, 0, streams, body, c.ws, c.cfg, ph, pred, row, c.st);
                 }
             }
-            return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), body, c.ws, c.cfg, phase,
+            return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), body, c.ws, c.cfg, ph,
                           pred, row, c.st);
         });
+        if (rc != KPL_OK || !c.ic0) return rc;
+        // IC(0): u = M r, then the reductions (x,x), (r,r), (r,u) of BodyInitR
+        if ((rc = ic0_apply(op, c.ic, c.ws.head, v->r, v->r, SEL_FIXED, v->u, pred, row, c.st)) != KPL_OK)
+            return rc;
+        if (phase == PH_NONE) return KPL_OK;
+        BodyPairs<3> red;
+        red.a[0] = v->x; red.b[0] = v->x; red.a[1] = v->r; red.b[1] = v->r; red.a[2] = v->r; red.b[2] = v->u;
+        return launch(op, L, InNone(), red, c.ws, c.cfg, phase, pred, row, c.st);
+    }
     case KPL_SW_INIT_W: {                // w = axpy(-sigma, r, A u) + first reductions (:376, :388-390)
         BodyInitW body;
         body.r = v->r; body.u = u; body.w = v->w0; body.sigma = c.sigma; body.ident = c.ident;
-        body.dinv = op->inv_diag; body.mout = c.ws.mbuf;
+        body.dinv = op->inv_diag; body.mout = op->precond == KPL_PC_JACOBI_VEC ? c.ws.mbuf : nullptr;
         if (tma) {
             const double *streams[1] = {v->r};
             return launch_tma(op, L, u, u, 0, streams, body, c.ws, c.cfg, phase, pred, row, c.st);
         }
-        return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, u, u, SEL_FIXED), body, c.ws, c.cfg, phase, pred, row,
-                      c.st);
+        rc = launch(op, L, in_vec<KPL_PC_IDENTITY>(op, u, u, SEL_FIXED), body, c.ws, c.cfg, phase, pred, row,
+                    c.st);
+        if (rc != KPL_OK || !c.ic0) return rc;
+        return ic0_apply(op, c.ic, c.ws.head, v->w0, v->w0, SEL_FIXED, c.ws.mbuf, pred, row, c.st);  // m = M w
     }
     case KPL_SW_TRUE: {                  // ||b - A x|| (:233-234, :401-402)
         BodyTrue body;
@@ -582,9 +641,9 @@ int do_sweep(const Ctx &c, int kind, long long row) {
         return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED), body, c.ws, c.cfg, phase, pred,
                       row, c.st);
     }
-    case KPL_SW_ITER:                    // the fused pipelined iteration (:408-421 + :388-390)
+    case KPL_SW_ITER: {                  // the fused pipelined iteration (:408-421 + :388-390)
         if (c.cfg.method == KPL_M_PCG_VAR_SH)
-            return with_pc(op, [&](auto pc) -> int {
+            rc = with_pc(op, [&](auto pc) -> int {
                 constexpr int PC = decltype(pc)::value;
                 BodyPcgIter<PC, true> body;
                 body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
@@ -592,8 +651,8 @@ int do_sweep(const Ctx &c, int kind, long long row) {
                 body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = 0.0; body.dsig = 0.0;
                 body.schedule = c.cfg.schedule; body.want_xi = 0;
                 body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
-                body.mout = c.ws.mbuf;
-                if constexpr (PC == KPL_PC_JACOBI_VEC) {
+                body.mout = c.ws.mbuf; body.mld = c.ws.mbuf;
+                if constexpr (PC == KPL_PC_JACOBI_VEC || PC == KPL_PC_IC0) {
                     if (c.ws.mbuf)
                         return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred,
                                       row, c.st, in_vec<KPL_PC_IDENTITY>(op, c.ws.mbuf, c.ws.mbuf, SEL_FIXED));
@@ -601,10 +660,10 @@ int do_sweep(const Ctx &c, int kind, long long row) {
                 return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred, row,
                               c.st);
             });
-        return with_pc(op, [&](auto pc) -> int {
+        else rc = with_pc(op, [&](auto pc) -> int {
             constexpr int PC = decltype(pc)::value;
             BodyPcgIter<PC> body;
-            body.schedule = nullptr; body.dsig = 0.0; body.mout = c.ws.mbuf;
+            body.schedule = nullptr; body.dsig = 0.0; body.mout = c.ws.mbuf; body.mld = c.ws.mbuf;
             body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
             body.s = v->s; body.t = v->t; body.p = v->p; body.w0 = v->w0; body.w1 = v->w1;
             body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = c.sigma;
@@ -622,7 +681,7 @@ int do_sweep(const Ctx &c, int kind, long long row) {
                                                           pred, row, c.st);
                 }
             }
-            if constexpr (PC == KPL_PC_JACOBI_VEC) {
+            if constexpr (PC == KPL_PC_JACOBI_VEC || PC == KPL_PC_IC0) {
                 if (c.ws.mbuf)      // SpMV on the materialised m (one gather per nonzero)
                     return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred,
                                   row, c.st, in_vec<KPL_PC_IDENTITY>(op, c.ws.mbuf, c.ws.mbuf, SEL_FIXED));
@@ -630,6 +689,10 @@ int do_sweep(const Ctx &c, int kind, long long row) {
             return launch(op, L, in_vec<PC>(op, v->w0, v->w1, SEL_ITER), body, c.ws, c.cfg, phase, pred, row,
                           c.st);
         });
+        if (rc != KPL_OK || !c.ic0) return rc;
+        // IC(0): m = M^-1 w of the w just written (the current w once the epilogue advanced iter)
+        return ic0_apply(op, c.ic, c.ws.head, v->w0, v->w1, SEL_ITER, c.ws.mbuf, pred, row, c.st);
+    }
     case KPL_SW_CG_P: {                  // p = axpy(beta, p, u); s = A p; delta = (s, p) (:269-271)
         InCgP in;
         in.p0 = v->p; in.p1 = v->p1; in.u = u; in.p = v->p; in.beta = 0.0;
@@ -637,26 +700,40 @@ int do_sweep(const Ctx &c, int kind, long long row) {
         bp.p0 = v->p; bp.p1 = v->p1; bp.s = v->s; bp.pout = v->p1;
         return launch(op, L, in, bp, c.ws, c.cfg, phase, pred, row, c.st);
     }
-    case KPL_SW_CG_X:                    // x, r, u updates + next head (:290-292, :258-259)
-        return with_pc(op, [&](auto pc) -> int {
+    case KPL_SW_CG_X: {                  // x, r, u updates + next head (:290-292, :258-259)
+        const int ph = c.ic0 ? PH_NONE : phase;
+        rc = with_pc(op, [&](auto pc) -> int {
             constexpr int PC = decltype(pc)::value;
             BodyCgX<PC> bx;
             bx.x = v->x; bx.r = v->r; bx.u = v->u; bx.p0 = v->p; bx.p1 = v->p1; bx.s = v->s;
             bx.dinv = op->inv_diag; bx.c = op->pc_const; bx.alpha = 0.0; bx.p = v->p;
-            return launch(op, L, InNone(), bx, c.ws, c.cfg, phase, pred, row, c.st);
+            return launch(op, L, InNone(), bx, c.ws, c.cfg, ph, pred, row, c.st);
         });
+        if (rc != KPL_OK || !c.ic0) return rc;
+        // IC(0): u = M r, then the head's reductions (r,u), (r,r)
+        if ((rc = ic0_apply(op, c.ic, c.ws.head, v->r, v->r, SEL_FIXED, v->u, pred, row, c.st)) != KPL_OK)
+            return rc;
+        BodyPairs<2> red;
+        red.a[0] = v->r; red.b[0] = v->u; red.a[1] = v->r; red.b[1] = v->r;
+        return launch(op, L, InNone(), red, c.ws, c.cfg, phase, pred, row, c.st);
+    }
     case KPL_SW_RR_W:                    // replacement w = A u (:602)
     case KPL_SW_RR_S:                    // replacement s = A p, q = M s (:603-604)
-        return with_pc(op, [&](auto pc) -> int {
+        rc = with_pc(op, [&](auto pc) -> int {
             constexpr int PC = decltype(pc)::value;
             BodyRepl<PC> rw;
             rw.mode = kind == KPL_SW_RR_W ? 0 : 1;
             rw.w0 = v->w0; rw.w1 = v->w1; rw.s = v->s; rw.q = v->q; rw.dinv = op->inv_diag;
-            rw.c = op->pc_const; rw.wout = v->w1; rw.mout = kind == KPL_SW_RR_W ? c.ws.mbuf : nullptr;
+            rw.c = op->pc_const; rw.wout = v->w1;
+            rw.mout = kind == KPL_SW_RR_W && op->precond == KPL_PC_JACOBI_VEC ? c.ws.mbuf : nullptr;
             const double *in = kind == KPL_SW_RR_W ? u : (c.ident ? v->t : v->p);
             return launch(op, L, in_vec<KPL_PC_IDENTITY>(op, in, in, SEL_FIXED), rw, c.ws, c.cfg, phase, pred,
                           row, c.st);
         });
+        if (rc != KPL_OK || !c.ic0) return rc;
+        if (kind == KPL_SW_RR_W)         // m = M w of the replaced w
+            return ic0_apply(op, c.ic, c.ws.head, v->w0, v->w1, SEL_ITER1, c.ws.mbuf, pred, row, c.st);
+        return ic0_apply(op, c.ic, c.ws.head, v->s, v->s, SEL_FIXED, v->q, pred, row, c.st);   // q = M s
     case KPL_SW_RR_Z: {                  // replacement z = A q + the next record's reductions (:605)
         BodyReplZ rz;
         rz.z = v->z; rz.r = v->r; rz.u = u; rz.w0 = v->w0; rz.w1 = v->w1; rz.ident = c.ident; rz.w = v->w0;
@@ -723,6 +800,10 @@ int kpl_solver_prepare(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v,
         zero_vec(c, v->s);
         zero_vec(c, v->t);
         if (!c.ident) { zero_vec(c, v->q); zero_vec(c, v->p); }
+    }
+    if (c.ic0) {                         // substitution sweeps start from cleared flags / tickets
+        cudaMemsetAsync(c.ic.fflag, 0, sizeof(int) * op->n, c.st);
+        cudaMemsetAsync(c.ic.tickets, 0, 2 * sizeof(unsigned int), c.st);
     }
     return cuda_check("prepare");
 }
@@ -879,6 +960,67 @@ int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfgp, int32_t kind, int
     g_launches.fetch_add(1, std::memory_order_relaxed);
     finalize_kernel<<<1, NT, 0, (cudaStream_t)stream>>>(ws, cfg, phase, pred, row);
     return cuda_check("finalize");
+}
+
+int64_t kpl_ic0_scratch_bytes(int64_t n) {
+    if (n < 1) return fail(KPL_EINVAL, "matrix dimension must be >= 1");
+    return align256(4LL * n) + 256;
+}
+
+int kpl_ic0_factor(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const double *a_values,
+                   double diag_scale, double *l_values, void *scratch, int64_t *bad_row, void *stream) {
+    if (n < 1 || !row_ptr || !col_idx || !a_values || !l_values || !scratch || !bad_row)
+        return fail(KPL_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    char *base = static_cast<char *>(scratch);
+    int *flag = reinterpret_cast<int *>(base);
+    unsigned int *ticket = reinterpret_cast<unsigned int *>(base + align256(4LL * n));
+    unsigned long long *bad = reinterpret_cast<unsigned long long *>(base + align256(4LL * n) + 8);
+    const unsigned long long none = ~0ULL;
+    cudaMemsetAsync(flag, 0, sizeof(int) * n, st);
+    cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+    cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, st);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    ic0_factor_kernel<<<(unsigned)cdiv(n, NT), NT, 0, st>>>(n, Tri{row_ptr, col_idx, nullptr}, a_values, diag_scale,
+                                                           l_values, flag, ticket, bad);
+    int rc = cuda_check("IC(0) factor");
+    if (rc != KPL_OK) return rc;
+    unsigned long long b = none;
+    cudaMemcpyAsync(&b, bad, sizeof(b), cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(KPL_ECUDA, std::string("IC(0) factor: ") + cudaGetErrorString(e));
+    *bad_row = b == none ? -1 : (int64_t)b;
+    return KPL_OK;
+}
+
+int kpl_precond_apply(const kpl_op *op, const double *v, double *out, void *workspace, void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if (!v || !out) return fail(KPL_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (op->precond) {
+    case KPL_PC_IDENTITY:
+        if (out != v) cudaMemcpyAsync(out, v, sizeof(double) * op->n, cudaMemcpyDeviceToDevice, st);
+        return cuda_check("identity apply");
+    case KPL_PC_JACOBI_CONST: case KPL_PC_JACOBI_VEC: {
+        const long long blocks = std::min<long long>(cdiv(op->n, 256), 148LL * 16);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        jacobi_kernel<<<(unsigned)blocks, 256, 0, st>>>(op->n, op->precond == KPL_PC_JACOBI_VEC ? op->inv_diag
+                                                                                               : nullptr,
+                                                        op->pc_const, v, out);
+        return cuda_check("Jacobi apply");
+    }
+    case KPL_PC_IC0: {
+        if (!workspace) return fail(KPL_EINVAL, "workspace required");
+        const Ic0Ws s = make_ic0_ws(op, L, 0, workspace);
+        cudaMemsetAsync(s.fflag, 0, sizeof(int) * op->n, st);
+        cudaMemsetAsync(s.tickets, 0, 2 * sizeof(unsigned int), st);
+        return ic0_apply(op, s, nullptr, v, v, SEL_FIXED, out, PRED_ALWAYS, 0, st);
+    }
+    default:
+        return fail(KPL_EINVAL, "unknown preconditioner");
+    }
 }
 
 int kpl_chunk_table(const kpl_op *op, void *workspace, void **local, void **global, int64_t *local_bytes) {

@@ -146,6 +146,7 @@ class DevicePrecond:
         kind = "identity" if M is None else getattr(M, "kind", "identity")
         self.inv_diag = None
         self.const = 0.0
+        self.ic = None
         if kind == "identity":
             self.code = _lib.KPL_PC_IDENTITY
         elif kind == "jacobi":
@@ -164,9 +165,15 @@ class DevicePrecond:
                 if len(inv) != dm.n:
                     raise ValueError("dimension mismatch in preconditioner apply")
                 self.inv_diag = t.from_numpy(np.ascontiguousarray(inv, dtype=np.float64)).to(device)
+        elif kind == "ic0":
+            if dm.kind != _lib.KPL_OP_CSR:
+                raise NotImplementedError("IC(0) runs with CSR operators (use A.to_csr())")
+            if M.ic.n != dm.n:
+                raise ValueError("dimension mismatch in preconditioner apply")
+            self.code = _lib.KPL_PC_IC0
+            self.ic = M.ic
         else:
-            raise NotImplementedError(
-                f"preconditioner kind {kind!r} is not on the device path (identity/jacobi only)")
+            raise NotImplementedError(f"preconditioner kind {kind!r} is not on the device path")
 
     @property
     def identity(self):
@@ -217,7 +224,15 @@ def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk
     if dp is not None:
         op.pc_const = dp.const
         op.inv_diag = ptr(dp.inv_diag)
+        if dp.ic is not None:
+            set_ic0(op, dp.ic)
     return op
+
+
+def set_ic0(op, ic):
+    """Point kpl_op's IC(0) fields at a device factor (precond.Ic0Factor)."""
+    op.ic_l_row_ptr, op.ic_l_col_idx, op.ic_l_values = ptr(ic.l_ptr), ptr(ic.l_col), ptr(ic.l_val)
+    op.ic_u_row_ptr, op.ic_u_col_idx, op.ic_u_values = ptr(ic.u_ptr), ptr(ic.u_col), ptr(ic.u_val)
 
 
 def vector_op(n) -> KplOp:

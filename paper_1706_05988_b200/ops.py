@@ -70,13 +70,32 @@ def axpy(alpha, x, y):
     return out.cpu().numpy() if host == "numpy" else (out.cpu() if host else out)
 
 
-def _jacobi_apply(M, v):
-    """v * inv_diag on the device (precond.py:88-89): axpy-free elementwise product."""
+def precond_apply(M, v):
+    """m = M^-1 v through kpl_precond_apply (precond.py:82-94): Jacobi
+    v * inv_diag, IC(0) the two substitution sweeps."""
     dev = D.require_cuda()
     t = D.torch()
-    vd, host = _vec(v, M.n, dev)
-    if M.inv_const is not None:
-        out = vd * float(M.inv_const)
+    vd, host = _vec(v, M.n, dev, "preconditioner input")
+    op = D.vector_op(M.n)
+    if M.kind == "jacobi":
+        if M.inv_const is not None:
+            op.precond, op.pc_const = _lib.KPL_PC_JACOBI_CONST, float(M.inv_const)
+        else:
+            inv = getattr(M, "_device", None)
+            if inv is None or inv.device != vd.device:
+                inv = t.from_numpy(np.ascontiguousarray(M.inv_diag, dtype=np.float64)).to(dev)
+                M._device = inv
+            op.precond, op.inv_diag = _lib.KPL_PC_JACOBI_VEC, D.ptr(inv)
+    elif M.kind == "ic0":
+        op.precond = _lib.KPL_PC_IC0
+        D.set_ic0(op, M.ic)
     else:
-        out = vd * t.from_numpy(np.ascontiguousarray(M.inv_diag)).to(dev)
+        raise ValueError(f"unknown preconditioner kind {M.kind!r}")
+    lib = _lib.load()
+    nb = lib.kpl_workspace_bytes(op, 0)
+    _lib.check(nb if nb < 0 else 0, "workspace size")
+    ws = t.empty(int(nb), dtype=t.uint8, device=dev)
+    out = t.empty_like(vd)
+    _lib.check(lib.kpl_precond_apply(op, D.ptr(vd), D.ptr(out), D.ptr(ws), D.stream_handle()),
+               "preconditioner apply")
     return out.cpu().numpy() if host == "numpy" else (out.cpu() if host else out)

@@ -1,12 +1,16 @@
 """Preconditioners of the drop-in API (mirror of pkg/src/kpl/precond.py).
 
-Only identity and Jacobi run on the device (the `north_star` path).  The
-reference's IC(0) (`make_ic0`, precond.py:134-154) is out of scope this
-round; passing an IC(0) preconditioner to a solver raises
-NotImplementedError rather than running anything on the CPU.
+identity, Jacobi and IC(0) all run on the device:
 
-`apply` is the device operation m = M^-1 v used inside the fused sweeps; the
-host-side `apply` here exists for API parity and computes on the device too.
+* Jacobi: m = v * inv_diag inside the fused sweeps (a constant for stencils);
+* IC(0) (`make_ic0`, precond.py:134-154): the factor is computed on the device
+  by a sync-free row sweep (kpl_ic0_factor, _kernels.py:77-115), and every
+  apply is the forward + backward substitution pair (kpl_ic0 sweeps,
+  _kernels.py:55-74) -- bit-identical to the reference.  Host work is index
+  bookkeeping only: the lower pattern, its transpose permutation, mu_tilde.
+
+`apply` is the device operation m = M^-1 v (kpl_precond_apply); inside the
+solvers the same kernels run between the fused sweeps.
 """
 
 from __future__ import annotations
@@ -23,21 +27,25 @@ class PreconditionerBreakdown(ArithmeticError):
 
 
 class Preconditioner:
-    """`kind` in {"identity", "jacobi"}; Jacobi keeps `inv_diag = 1 / diag(A)`.
+    """`kind` in {"identity", "jacobi", "ic0"}; Jacobi keeps `inv_diag = 1 / diag(A)`.
 
     For matrix-free stencils the diagonal is constant, so `inv_const` holds
     the single value fl(1/diag) and `inv_diag` is materialised only on access.
+    IC(0) keeps its factor on the device (`ic`, an `Ic0Factor`).
     """
 
-    __slots__ = ("kind", "_inv_diag", "inv_const", "n_rows", "mu_tilde", "_device")
+    __slots__ = ("kind", "_inv_diag", "inv_const", "n_rows", "mu_tilde", "_device", "ic",
+                 "_norm_estimate", "__weakref__")
 
-    def __init__(self, kind, inv_diag=None, inv_const=None, n=None):
+    def __init__(self, kind, inv_diag=None, inv_const=None, n=None, ic=None, mu_tilde=1):
         self.kind = kind
         self._inv_diag = None if inv_diag is None else np.ascontiguousarray(inv_diag, dtype=np.float64)
         self.inv_const = inv_const
         self.n_rows = n if n is not None else (None if inv_diag is None else len(inv_diag))
-        self.mu_tilde = 1
+        self.mu_tilde = mu_tilde
         self._device = None
+        self.ic = ic
+        self._norm_estimate = None
 
     @property
     def inv_diag(self):
@@ -49,19 +57,44 @@ class Preconditioner:
     def n(self):
         return self.n_rows
 
+    @property
+    def _l(self):
+        """Host (row_ptr, col_idx, l_values) of the IC(0) factor (the
+        reference's `Preconditioner._l`)."""
+        return None if self.ic is None else self.ic.host_lower()
+
+    def host_lower(self):
+        return self._l
+
     def apply(self, v):
-        """M^-1 v.  Identity returns v itself (precond.py:84-85)."""
+        """M^-1 v on the device.  Identity returns v itself (precond.py:84-85)."""
         if self.kind == "identity":
             return v
-        from .ops import _jacobi_apply
-        return _jacobi_apply(self, v)
+        from .ops import precond_apply
+        return precond_apply(self, v)
 
     def norm_estimate(self):
+        """precond.py:96-118: 1 (identity), max(inv_diag) (Jacobi), or 20
+        power-iteration steps on the applied operator (IC(0), device ops)."""
         if self.kind == "identity":
             return 1.0
-        if self.inv_const is not None:
-            return float(self.inv_const)
-        return float(self.inv_diag.max())
+        if self.kind == "jacobi":
+            if self.inv_const is not None:
+                return float(self.inv_const)
+            return float(self.inv_diag.max())
+        if self._norm_estimate is None:
+            from .ops import dot, norm2
+            v = np.full(self.n, 1.0 / np.sqrt(self.n))
+            lam = 1.0
+            for _ in range(20):
+                w = self.apply(v)
+                lam = dot(v, w)
+                nw = norm2(w)
+                if nw == 0.0:
+                    break
+                v = w / nw
+            self._norm_estimate = abs(float(lam))
+        return self._norm_estimate
 
     def __repr__(self):
         return f"Preconditioner(kind={self.kind!r}, n={self.n})"
@@ -85,7 +118,82 @@ def make_jacobi(A) -> Preconditioner:
     return Preconditioner("jacobi", inv_diag=1.0 / d)
 
 
-def make_ic0(A, eta: float = 0.0):
-    raise NotImplementedError(
-        "IC(0) is outside this build's device scope (SURVEY.md 8f-4); "
-        "use identity() or make_jacobi()")
+class Ic0Factor:
+    """Device-resident IC(0) factor: L (lower CSR, diagonal last) and
+    U = L^T (diagonal first), int32 indices, fp64 values."""
+
+    def __init__(self, n, l_ptr, l_col, l_val, u_ptr, u_col, u_val, host_ptr, host_col):
+        self.n = n
+        self.l_ptr, self.l_col, self.l_val = l_ptr, l_col, l_val
+        self.u_ptr, self.u_col, self.u_val = u_ptr, u_col, u_val
+        self._host = (host_ptr, host_col)
+
+    def host_lower(self):
+        ptr, col = self._host
+        return ptr, col, self.l_val.cpu().numpy()
+
+
+def _lower_pattern(A):
+    """precond.py:28-43 index part: the lower triangle's row pointer, columns
+    and the positions of its entries in A.values (diagonal last per row)."""
+    n = A.n
+    row_ptr = np.asarray(A.row_ptr, dtype=np.int64)
+    col_idx = np.asarray(A.col_idx, dtype=np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(row_ptr))
+    keep = np.flatnonzero(col_idx <= rows)
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[keep], minlength=n), out=ptr[1:])
+    cols = col_idx[keep]
+    last = ptr[1:] - 1
+    if np.any(ptr[1:] == ptr[:-1]) or np.any(cols[last] != np.arange(n)):
+        raise ValueError("matrix has a structurally missing diagonal entry")
+    return ptr, cols, keep
+
+
+def _transpose_perm(n, ptr, cols):
+    """precond.py:46-53 index part: CSR pattern of the transpose and the
+    permutation taking the factor's values to it (rows of a column ascending)."""
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr))
+    perm = np.lexsort((rows, cols))
+    tptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(cols, minlength=n), out=tptr[1:])
+    return tptr, rows[perm], perm
+
+
+def make_ic0(A, eta: float = 0.0) -> Preconditioner:
+    """precond.py:134-154: IC(0) of A + eta*diag(diag(A)) on the pattern of
+    lower(A), factored on the device.  Raises PreconditionerBreakdown(row)
+    for the first non-positive pivot."""
+    if eta < 0.0:
+        raise ValueError("compensation shift eta must be >= 0")
+    from . import _lib
+    from . import device as D
+    if hasattr(A, "stencil_spec"):
+        A = A.to_csr()
+    ptr, cols, keep = _lower_pattern(A)
+    n, nnz = A.n, len(cols)
+    if nnz >= 2**31:
+        raise ValueError("factor too large for int32 indices")
+    dev = D.require_cuda()
+    t = D.torch()
+    i32 = lambda a: t.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev)
+    l_ptr, l_col = i32(ptr), i32(cols)
+    a_val = t.from_numpy(np.ascontiguousarray(np.asarray(A.values)[keep], dtype=np.float64)).to(dev)
+    l_val = t.empty(nnz, dtype=t.float64, device=dev)
+    lib = _lib.load()
+    scratch = t.empty(int(lib.kpl_ic0_scratch_bytes(n)), dtype=t.uint8, device=dev)
+    bad = _lib._i64(-1)
+    import ctypes
+    _lib.check(lib.kpl_ic0_factor(n, D.ptr(l_ptr), D.ptr(l_col), D.ptr(a_val), 1.0 + eta, D.ptr(l_val),
+                                  D.ptr(scratch), ctypes.byref(bad), D.stream_handle()), "IC(0) factor")
+    if bad.value >= 0:
+        raise PreconditionerBreakdown(int(bad.value))
+    tptr, trows, perm = _transpose_perm(n, ptr, cols)
+    u_val = t.empty(nnz, dtype=t.float64, device=dev)
+    perm_d = i32(perm)
+    _lib.check(lib.kpl_gather(nnz, D.ptr(perm_d), D.ptr(l_val), D.ptr(u_val), D.stream_handle()),
+               "IC(0) transpose")
+    counts = np.diff(ptr)
+    mu_tilde = int((counts + np.bincount(cols, minlength=n) - 1).max())
+    ic = Ic0Factor(n, l_ptr, l_col, l_val, i32(tptr), i32(trows), u_val, ptr, cols)
+    return Preconditioner("ic0", n=n, ic=ic, mu_tilde=mu_tilde)

@@ -160,6 +160,15 @@ class SolverState:
 
 # ------------------------------------------------------------------ engine
 
+def _assembled(A):
+    """CSR form of a matrix-free stencil, built once per stencil object."""
+    csr = getattr(A, "_csr", None)
+    if csr is None:
+        csr = A.to_csr()
+        A._csr = csr
+    return csr
+
+
 class _Solve:
     """One solve: device vectors, workspace, and the host enqueue loop."""
 
@@ -174,6 +183,8 @@ class _Solve:
         t = D.torch()
         self.cfg = cfg
         self.A = A
+        if getattr(M, "kind", None) == "ic0" and hasattr(A, "stencil_spec"):
+            A = _assembled(A)            # IC(0) runs with the CSR form (bitwise the same operator)
         self.dm = D.device_matrix(A, dev)
         self.dp = D.device_precond(M, self.dm, dev)
         n = self.n = self.dm.n

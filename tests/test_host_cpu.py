@@ -161,8 +161,11 @@ def test_jacobi_stencil_is_constant():
     assert M.inv_const == 1.0 / 6.0 and np.all(M.inv_diag == 1.0 / 6.0)
     M2 = K.make_jacobi(K.laplacian_2d(3, 3))
     assert np.all(M2.inv_diag == 0.25)
-    with pytest.raises(NotImplementedError):
+    # IC(0) is factored on the device: without a GPU it fails loudly (no CPU fallback)
+    with pytest.raises(_lib.KplError, match="no CUDA device"):
         K.make_ic0(K.laplacian_2d(3, 3))
+    with pytest.raises(ValueError):
+        K.make_ic0(K.laplacian_2d(3, 3), eta=-1.0)
 
 
 # ---------------------------------------------------- GPU-order emulator
