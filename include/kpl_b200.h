@@ -93,6 +93,10 @@ typedef struct kpl_op {
     const int32_t *ic_u_row_ptr;
     const int32_t *ic_u_col_idx;
     const double  *ic_u_values;
+    /* row processing orders of the two substitution sweeps: any topological
+       order (from kpl_ic0_levels, rows sorted by level); NULL = natural     */
+    const int32_t *ic_l_order;
+    const int32_t *ic_u_order;
 } kpl_op;
 
 #define KPL_ORDER_TREE      0
@@ -237,16 +241,24 @@ int kpl_sweep_phase(int32_t kind);
 /* ---- IC(0) preconditioner (reference: precond.py:134-154, _kernels.py:55-115)
    The factor and both substitutions run as sync-free row sweeps on the
    device, bit-identical to the reference's sequential loops.              */
-/* Scratch bytes kpl_ic0_factor needs for an n-row factor.                  */
+/* Scratch bytes kpl_ic0_factor / kpl_ic0_levels need for n rows.          */
 int64_t kpl_ic0_scratch_bytes(int64_t n);
+/* level[i] = 1 + max level of the rows row i depends on (0 if none): upper
+   = 0 for L (columns < i, diagonal last), 1 for L^T (columns > i, diagonal
+   first).  Sorting rows by level gives the processing order the sweeps
+   use (kpl_op.ic_*_order); it does not change any value computed.         */
+int kpl_ic0_levels(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, int32_t upper, int32_t *level,
+                   void *scratch, void *stream);
 /* l_values = IC(0) factor of the lower pattern (row_ptr, col_idx; diagonal
-   last) whose values are a_values (A's lower triangle); each diagonal entry
+   last; rows processed in `order`, NULL = natural) whose values are a_values
+   (A's lower triangle); each diagonal entry
    is multiplied by diag_scale = 1 + eta first (precond.py:41-42; x * 1.0 is
    exact, so eta = 0 needs no special case).  *bad_row (host) = -1, or the
    first row whose pivot is not positive (_kernels.py:112-113 ->
    PreconditionerBreakdown).  Blocks until the factor is done.              */
-int kpl_ic0_factor(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const double *a_values,
-                   double diag_scale, double *l_values, void *scratch, int64_t *bad_row, void *stream);
+int kpl_ic0_factor(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const int32_t *order,
+                   const double *a_values, double diag_scale, double *l_values, void *scratch, int64_t *bad_row,
+                   void *stream);
 /* out = M^-1 v for the operator's preconditioner (identity: copy; Jacobi:
    v * inv_diag; IC(0): upper_solve(lower_solve(v))) -- precond.py:82-94.
    `workspace`: kpl_workspace_bytes(op, 0) bytes.                           */

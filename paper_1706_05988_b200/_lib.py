@@ -41,7 +41,8 @@ class KplOp(ctypes.Structure):
                 ("chunk_blocks", _i32), ("zhalo", _i32), ("pc_const", _d), ("inv_diag", _p),
                 ("chunk_offset", _i64), ("chunks_global", _i64), ("order", _i32), ("_reserved", _i32),
                 ("ic_l_row_ptr", _p), ("ic_l_col_idx", _p), ("ic_l_values", _p),
-                ("ic_u_row_ptr", _p), ("ic_u_col_idx", _p), ("ic_u_values", _p)]
+                ("ic_u_row_ptr", _p), ("ic_u_col_idx", _p), ("ic_u_values", _p),
+                ("ic_l_order", _p), ("ic_u_order", _p)]
 
 
 class KplCfg(ctypes.Structure):
@@ -90,7 +91,8 @@ _SIGS = {
                          _i32, _i64, _p, _p]),
     "kpl_sweep_phase": (_i32, [_i32]),
     "kpl_ic0_scratch_bytes": (_i64, [_i64]),
-    "kpl_ic0_factor": (_i32, [_i64, _p, _p, _p, _d, _p, _p, ctypes.POINTER(_i64), _p]),
+    "kpl_ic0_levels": (_i32, [_i64, _p, _p, _i32, _p, _p, _p]),
+    "kpl_ic0_factor": (_i32, [_i64, _p, _p, _p, _p, _d, _p, _p, ctypes.POINTER(_i64), _p]),
     "kpl_precond_apply": (_i32, [ctypes.POINTER(KplOp), _p, _p, _p, _p]),
     "kpl_chunk_table": (_i32, [ctypes.POINTER(KplOp), _p, ctypes.POINTER(_p), ctypes.POINTER(_p),
                                ctypes.POINTER(_i64)]),

@@ -116,8 +116,8 @@ Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     o.mbuf = o.nbuf + (op->kind == KPL_OP_CSR && op->row_ptr ? align256(8LL * op->n) : 0);
     o.prod = o.mbuf + (use_mbuf(op) ? align256(8LL * op->n) : 0);
     o.ic0 = o.prod + (ordered(op) ? align256(8LL * NQ * op->n) : 0);
-    // IC(0): y = L^-1 v, forward / backward row flags, two tickets
-    o.total = o.ic0 + (is_ic0(op) ? align256(8LL * op->n) + 2 * align256(4LL * op->n) + 256 : 0);
+    // IC(0): y = L^-1 v, two tickets
+    o.total = o.ic0 + (is_ic0(op) ? align256(8LL * op->n) + 256 : 0);
     return o;
 }
 
@@ -147,14 +147,16 @@ Ic0Ws make_ic0_ws(const kpl_op *op, const Layout &L, long long max_iters, void *
     const Offsets o = offsets(op, L, max_iters);
     char *base = static_cast<char *>(workspace) + o.ic0;
     s.y = reinterpret_cast<double *>(base);
-    s.fflag = reinterpret_cast<int *>(base + align256(8LL * op->n));
-    s.bflag = reinterpret_cast<int *>(base + align256(8LL * op->n) + align256(4LL * op->n));
-    s.tickets = reinterpret_cast<unsigned int *>(base + align256(8LL * op->n) + 2 * align256(4LL * op->n));
+    s.tickets = reinterpret_cast<unsigned int *>(base + align256(8LL * op->n));
     return s;
 }
 
-Tri ic0_lower(const kpl_op *op) { return Tri{op->ic_l_row_ptr, op->ic_l_col_idx, op->ic_l_values}; }
-Tri ic0_upper(const kpl_op *op) { return Tri{op->ic_u_row_ptr, op->ic_u_col_idx, op->ic_u_values}; }
+Tri ic0_lower(const kpl_op *op) {
+    return Tri{op->ic_l_row_ptr, op->ic_l_col_idx, op->ic_l_values, op->ic_l_order};
+}
+Tri ic0_upper(const kpl_op *op) {
+    return Tri{op->ic_u_row_ptr, op->ic_u_col_idx, op->ic_u_values, op->ic_u_order};
+}
 
 // out = U^-1 L^-1 pick(v0, v1): the two sync-free substitution sweeps
 int ic0_apply(const kpl_op *op, const Ic0Ws &s, const WsHead *head, const double *v0, const double *v1,
@@ -162,9 +164,17 @@ int ic0_apply(const kpl_op *op, const Ic0Ws &s, const WsHead *head, const double
     if (!op->ic_l_row_ptr || !op->ic_u_row_ptr) return fail(KPL_EINVAL, "IC(0) factor arrays missing");
     const unsigned grid = (unsigned)cdiv(op->n, NT);
     g_launches.fetch_add(2, std::memory_order_relaxed);
-    ic0_lower_kernel<<<grid, NT, 0, st>>>(op->n, ic0_lower(op), v0, v1, sel, s, head, pred, row);
+    ic0_lower_kernel<<<grid, NT, 0, st>>>(op->n, ic0_lower(op), v0, v1, sel, out, s, head, pred, row);
     ic0_upper_kernel<<<grid, NT, 0, st>>>(op->n, ic0_upper(op), out, s, head, pred, row);
     return cuda_check("IC(0) apply");
+}
+
+// y := empty, tickets := 0 (before the first apply on a workspace)
+int ic0_reset(const kpl_op *op, const Ic0Ws &s, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    ic0_empty_kernel<<<(unsigned)std::min<long long>(cdiv(op->n, 256), 148LL * 8), 256, 0, st>>>(op->n, s.y);
+    cudaMemsetAsync(s.tickets, 0, 2 * sizeof(unsigned int), st);
+    return cuda_check("IC(0) reset");
 }
 
 Cfg make_cfg(const kpl_cfg *c) {
@@ -801,9 +811,9 @@ int kpl_solver_prepare(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v,
         zero_vec(c, v->t);
         if (!c.ident) { zero_vec(c, v->q); zero_vec(c, v->p); }
     }
-    if (c.ic0) {                         // substitution sweeps start from cleared flags / tickets
-        cudaMemsetAsync(c.ic.fflag, 0, sizeof(int) * op->n, c.st);
-        cudaMemsetAsync(c.ic.tickets, 0, 2 * sizeof(unsigned int), c.st);
+    if (c.ic0) {                         // substitution sweeps start from an empty y, fresh tickets
+        const int rc2 = ic0_reset(op, c.ic, c.st);
+        if (rc2 != KPL_OK) return rc2;
     }
     return cuda_check("prepare");
 }
@@ -967,8 +977,24 @@ int64_t kpl_ic0_scratch_bytes(int64_t n) {
     return align256(4LL * n) + 256;
 }
 
-int kpl_ic0_factor(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const double *a_values,
-                   double diag_scale, double *l_values, void *scratch, int64_t *bad_row, void *stream) {
+int kpl_ic0_levels(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, int32_t upper, int32_t *level,
+                   void *scratch, void *stream) {
+    if (n < 1 || !row_ptr || !col_idx || !level || !scratch) return fail(KPL_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    char *base = static_cast<char *>(scratch);
+    int *flag = reinterpret_cast<int *>(base);
+    unsigned int *ticket = reinterpret_cast<unsigned int *>(base + align256(4LL * n));
+    cudaMemsetAsync(flag, 0, sizeof(int) * n, st);
+    cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    ic0_levels_kernel<<<(unsigned)cdiv(n, NT), NT, 0, st>>>(n, Tri{row_ptr, col_idx, nullptr, nullptr},
+                                                           upper ? 1 : 0, level, flag, ticket);
+    return cuda_check("IC(0) levels");
+}
+
+int kpl_ic0_factor(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const int32_t *order,
+                   const double *a_values, double diag_scale, double *l_values, void *scratch, int64_t *bad_row,
+                   void *stream) {
     if (n < 1 || !row_ptr || !col_idx || !a_values || !l_values || !scratch || !bad_row)
         return fail(KPL_EINVAL, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
@@ -981,7 +1007,7 @@ int kpl_ic0_factor(int64_t n, const int32_t *row_ptr, const int32_t *col_idx, co
     cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
     cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, st);
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    ic0_factor_kernel<<<(unsigned)cdiv(n, NT), NT, 0, st>>>(n, Tri{row_ptr, col_idx, nullptr}, a_values, diag_scale,
+    ic0_factor_kernel<<<(unsigned)cdiv(n, NT), NT, 0, st>>>(n, Tri{row_ptr, col_idx, nullptr, order}, a_values, diag_scale,
                                                            l_values, flag, ticket, bad);
     int rc = cuda_check("IC(0) factor");
     if (rc != KPL_OK) return rc;
@@ -1014,8 +1040,7 @@ int kpl_precond_apply(const kpl_op *op, const double *v, double *out, void *work
     case KPL_PC_IC0: {
         if (!workspace) return fail(KPL_EINVAL, "workspace required");
         const Ic0Ws s = make_ic0_ws(op, L, 0, workspace);
-        cudaMemsetAsync(s.fflag, 0, sizeof(int) * op->n, st);
-        cudaMemsetAsync(s.tickets, 0, 2 * sizeof(unsigned int), st);
+        if ((rc = ic0_reset(op, s, st)) != KPL_OK) return rc;
         return ic0_apply(op, s, nullptr, v, v, SEL_FIXED, out, PRED_ALWAYS, 0, st);
     }
     default:

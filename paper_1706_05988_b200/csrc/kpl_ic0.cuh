@@ -4,17 +4,19 @@
 //
 // All three are row-sequential recurrences whose dependencies follow the
 // sparsity pattern.  They run as *sync-free* sweeps: one thread per row, each
-// row waits (acquire-spin) on a per-row ready flag of every row it reads, then
-// publishes its own value with a release store.  Rows are handed to CTAs by
-// an atomic ticket in dependency order (ascending for L, descending for L^T),
-// so a CTA only ever waits on rows owned by CTAs that are already resident --
-// no deadlock regardless of grid size.  Inside a row the arithmetic is the
+// row waits until every row it reads has been published, then publishes its
+// own (the substitutions: the value itself, see kIcEmpty; the factor: a
+// per-row flag with release/acquire, since a row there is many values).  Rows are handed to CTAs by an atomic ticket
+// in a topological order -- the rows sorted by dependency level (computed
+// once per factor by ic0_levels_kernel), so the resident CTAs hold whole
+// wavefronts instead of a contiguous band of rows, and a CTA only ever waits
+// on rows owned by CTAs that are already resident: no deadlock regardless of
+// grid size.  (NULL order = natural order, ascending for L, descending for
+// L^T, also topological.)  Inside a row the arithmetic is the
 // reference's, term for term (--fmad=false, explicit __d*_rn), so the factor
 // and every apply are bit-identical to the reference.
-//
-// Flags are never reset by a separate pass: the forward sweep clears the
-// backward flags of the rows it finishes and vice versa (the other sweep is
-// complete by stream order), and each sweep re-arms the other's ticket.
+// Each sweep re-arms the other's ticket (the other sweep is complete by
+// stream order), so nothing is reset between applies.
 #pragma once
 #include "kpl_bodies.cuh"
 
@@ -30,26 +32,79 @@ __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+#ifndef KPL_IC0_SPIN_NS
+#define KPL_IC0_SPIN_NS 20
+#endif
+
+__device__ __forceinline__ int ld_relaxed(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Spin with relaxed loads, then one acquire load: an acquire load also
+// invalidates the SM's L1 (CCTL.IVALL), so spinning on it would evict the
+// data every other warp on the SM is reading.
 __device__ __forceinline__ void wait_flag(const int *f) {
-    while (ld_acquire(f) == 0) __nanosleep(20);
+    while (ld_relaxed(f) == 0) {
+        if (KPL_IC0_SPIN_NS > 0) __nanosleep(KPL_IC0_SPIN_NS);
+    }
+    (void)ld_acquire(f);
 }
 
 struct Tri {                // CSR triangle, int32 indices
     const int *rp, *ci;
     const double *v;
+    const int *order;       // processing order (topological), NULL = natural
 };
 
+// Row handled by slot t of a sweep (upper sweeps run the natural order backwards).
+__device__ __forceinline__ long long tri_row(const Tri &T, long long t, long long n, bool upper) {
+    if (T.order) return __ldg(T.order + t);
+    return upper ? n - 1 - t : t;
+}
+
 struct Ic0Ws {              // apply scratch inside the solver workspace
-    double *y;              // L^-1 v
-    int *fflag, *bflag;     // per-row ready flags of the two sweeps
+    double *y;              // L^-1 v (holds kIcEmpty between applies)
     unsigned int *tickets;  // [0] forward, [1] backward
 };
+
+// The substitution sweeps publish each row's value by storing the value
+// itself: every not-yet-computed entry holds kIcEmpty, a *signalling* NaN.
+// IEEE arithmetic never returns a signalling NaN (an sNaN operand comes back
+// quieted), and every published value is a quotient, so a reader that sees
+// anything else sees the final value -- one relaxed 8-byte store per row, no
+// flag, no fence, no second load.  The forward sweep empties `out` row by row
+// for the backward sweep; the backward sweep empties y for the next forward
+// sweep (each after reading its own entry).
+constexpr unsigned long long kIcEmpty = 0x7ff4000000b1c0deULL;
+
+__device__ __forceinline__ double ld_relaxed_f64(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return __longlong_as_double((long long)v);
+}
+
+__device__ __forceinline__ void st_relaxed_f64(double *p, double x) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(x)) : "memory");
+}
+
+__device__ __forceinline__ double wait_value(const double *p) {
+    double x = ld_relaxed_f64(p);
+    while ((unsigned long long)__double_as_longlong(x) == kIcEmpty) {
+        if (KPL_IC0_SPIN_NS > 0) __nanosleep(KPL_IC0_SPIN_NS);
+        x = ld_relaxed_f64(p);
+    }
+    return x;
+}
+
+__device__ __forceinline__ double ic_empty() { return __longlong_as_double((long long)kIcEmpty); }
 
 // y = L^-1 v  (lower_solve, _kernels.py:55-63): acc = v[i]; acc -= l*y[c] in
 // stored order; y[i] = acc / l[diag].  `v` = pick(head, sel, v0, v1).
 __global__ void __launch_bounds__(NT) ic0_lower_kernel(long long n, Tri L, const double *v0, const double *v1,
-                                                       int sel, Ic0Ws s, const WsHead *head, int pred,
-                                                       long long row) {
+                                                       int sel, double *out, Ic0Ws s, const WsHead *head,
+                                                       int pred, long long row) {
     if (!pred_ok(head, pred, row)) return;
     __shared__ unsigned int s_blk;
     if (threadIdx.x == 0) {
@@ -57,19 +112,16 @@ __global__ void __launch_bounds__(NT) ic0_lower_kernel(long long n, Tri L, const
         if (s_blk == 0) s.tickets[1] = 0u;             // re-arm the backward sweep
     }
     __syncthreads();
-    const long long i = (long long)s_blk * NT + threadIdx.x;
-    if (i >= n) return;
+    const long long t = (long long)s_blk * NT + threadIdx.x;
+    if (t >= n) return;
+    const long long i = tri_row(L, t, n, false);
     const double *v = pick(head, sel, v0, v1);
     const int lo = L.rp[i], di = L.rp[i + 1] - 1;
     double acc = v[i];
-    for (int k = lo; k < di; ++k) {
-        const int c = L.ci[k];
-        wait_flag(s.fflag + c);
-        acc = __dsub_rn(acc, __dmul_rn(L.v[k], __ldcg(s.y + c)));
-    }
-    __stcg(s.y + i, __ddiv_rn(acc, L.v[di]));
-    s.bflag[i] = 0;
-    st_release(s.fflag + i, 1);
+    out[i] = ic_empty();                               // (after reading v[i]: out may alias v)
+    for (int k = lo; k < di; ++k)
+        acc = __dsub_rn(acc, __dmul_rn(L.v[k], wait_value(s.y + L.ci[k])));
+    st_relaxed_f64(s.y + i, __ddiv_rn(acc, L.v[di]));
 }
 
 // out = U^-1 y with U = L^T stored by rows, diagonal first (upper_solve,
@@ -83,19 +135,21 @@ __global__ void __launch_bounds__(NT) ic0_upper_kernel(long long n, Tri U, doubl
         if (s_blk == 0) s.tickets[0] = 0u;             // re-arm the forward sweep
     }
     __syncthreads();
-    const long long j = (long long)s_blk * NT + threadIdx.x;
-    if (j >= n) return;
-    const long long i = n - 1 - j;
+    const long long t = (long long)s_blk * NT + threadIdx.x;
+    if (t >= n) return;
+    const long long i = tri_row(U, t, n, true);
     const int di = U.rp[i], hi = U.rp[i + 1];
     double acc = __ldcg(s.y + i);
-    for (int k = di + 1; k < hi; ++k) {
-        const int c = U.ci[k];
-        wait_flag(s.bflag + c);
-        acc = __dsub_rn(acc, __dmul_rn(U.v[k], __ldcg(out + c)));
-    }
-    __stcg(out + i, __ddiv_rn(acc, U.v[di]));
-    s.fflag[i] = 0;
-    st_release(s.bflag + i, 1);
+    s.y[i] = ic_empty();
+    for (int k = di + 1; k < hi; ++k)
+        acc = __dsub_rn(acc, __dmul_rn(U.v[k], wait_value(out + U.ci[k])));
+    st_relaxed_f64(out + i, __ddiv_rn(acc, U.v[di]));
+}
+
+// Fill y with kIcEmpty (workspace preparation).
+__global__ void ic0_empty_kernel(long long n, double *y) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += gridDim.x * (long long)blockDim.x)
+        y[k] = ic_empty();
 }
 
 // IC(0) factor (ic0_factor, _kernels.py:77-115) on the lower pattern of A
@@ -110,8 +164,9 @@ __global__ void __launch_bounds__(NT) ic0_factor_kernel(long long n, Tri P, cons
     __shared__ unsigned int s_blk;
     if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
     __syncthreads();
-    const long long i = (long long)s_blk * NT + threadIdx.x;
-    if (i >= n) return;
+    const long long t = (long long)s_blk * NT + threadIdx.x;
+    if (t >= n) return;
+    const long long i = tri_row(P, t, n, false);
     const int lo = P.rp[i], di = P.rp[i + 1] - 1;
     for (int kk = lo; kk < di; ++kk) {
         const int c = P.ci[kk];
@@ -141,6 +196,29 @@ __global__ void __launch_bounds__(NT) ic0_factor_kernel(long long n, Tri P, cons
         d = __dsqrt_rn(d);
     }
     __stcg(l + di, d);
+    st_release(flag + i, 1);
+}
+
+// Dependency levels of a triangle's rows: level[i] = 1 + max level of the
+// rows it reads (0 if none), natural order, sync-free.  upper = 0: row i of
+// L reads columns < i (diagonal last); upper = 1: row i of L^T reads columns
+// > i (diagonal first), rows visited from n-1 down.
+__global__ void __launch_bounds__(NT) ic0_levels_kernel(long long n, Tri P, int upper, int *level, int *flag,
+                                                        unsigned int *ticket) {
+    __shared__ unsigned int s_blk;
+    if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const long long t = (long long)s_blk * NT + threadIdx.x;
+    if (t >= n) return;
+    const long long i = upper ? n - 1 - t : t;
+    const int lo = upper ? P.rp[i] + 1 : P.rp[i], hi = upper ? P.rp[i + 1] : P.rp[i + 1] - 1;
+    int lv = 0;
+    for (int k = lo; k < hi; ++k) {
+        const int c = P.ci[k];
+        wait_flag(flag + c);
+        lv = max(lv, __ldcg(level + c) + 1);
+    }
+    __stcg(level + i, lv);
     st_release(flag + i, 1);
 }
 

@@ -233,6 +233,7 @@ def set_ic0(op, ic):
     """Point kpl_op's IC(0) fields at a device factor (precond.Ic0Factor)."""
     op.ic_l_row_ptr, op.ic_l_col_idx, op.ic_l_values = ptr(ic.l_ptr), ptr(ic.l_col), ptr(ic.l_val)
     op.ic_u_row_ptr, op.ic_u_col_idx, op.ic_u_values = ptr(ic.u_ptr), ptr(ic.u_col), ptr(ic.u_val)
+    op.ic_l_order, op.ic_u_order = ptr(ic.l_order), ptr(ic.u_order)
 
 
 def vector_op(n) -> KplOp:
