@@ -91,7 +91,13 @@ int make_layout(const kpl_op *op, Layout &L) {
     return fail(KPL_EINVAL, "unknown operator kind");
 }
 
-struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, mbuf, prod, ic0, total; };
+struct Offsets { long long items, chunks, cnt, hist, reps, nbuf, mbuf, prod, ic0, pheads, total; };
+
+// Persistent redundant-epilogue kernel (small single-GPU stencils): one head +
+// scratch history row per CTA beyond the first (CTA 0 uses the real head).
+constexpr long long kPersistMaxCtas = 2LL * kSMs;
+constexpr long long kPheadBytes = 1024 + 256;
+bool has_pheads(const kpl_op *op) { return op->kind == KPL_OP_STENCIL && op->chunks_global <= 0; }
 
 bool is_ic0(const kpl_op *op) { return op->precond == KPL_PC_IC0; }
 
@@ -107,8 +113,8 @@ bool use_mbuf(const kpl_op *op) {
 Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     Offsets o;
     const long long cg = op->chunks_global > 0 ? op->chunks_global : L.nch;
-    o.items = 1024;
-    o.chunks = o.items + align256(8LL * NQ * L.items);
+    o.items = 1024;                    // two item buffers (the persistent kernel alternates them)
+    o.chunks = o.items + 2 * align256(8LL * NQ * L.items);
     o.cnt = o.chunks + align256(8LL * NQ * cg);
     o.hist = o.cnt + align256(4LL * L.nch);
     o.reps = o.hist + align256(8LL * HC * (max_iters + 1));
@@ -117,7 +123,8 @@ Offsets offsets(const kpl_op *op, const Layout &L, long long max_iters) {
     o.prod = o.mbuf + (use_mbuf(op) ? align256(8LL * op->n) : 0);
     o.ic0 = o.prod + (ordered(op) ? align256(8LL * NQ * op->n) : 0);
     // IC(0): y = L^-1 v, two tickets
-    o.total = o.ic0 + (is_ic0(op) ? align256(8LL * op->n) + 256 : 0);
+    o.pheads = o.ic0 + (is_ic0(op) ? align256(8LL * op->n) + 256 : 0);
+    o.total = o.pheads + (has_pheads(op) ? kPersistMaxCtas * kPheadBytes : 0);
     return o;
 }
 
@@ -138,6 +145,7 @@ Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspa
     ws.inline_final = op->chunks_global > 0 || ordered(op) ? 0 : 1;
     ws.prod = ordered(op) ? reinterpret_cast<double *>(base + o.prod) : nullptr;
     ws.nprod = op->n;
+    ws.hist_scratch = 0;
     return ws;
 }
 
@@ -370,6 +378,7 @@ __global__ void head_init_kernel(WsHead *h, double *hist, long long nrows, unsig
         h->final_cnt = 0u;
         h->bar_cnt = 0u;
         h->bar_gen = 0u;
+        h->bar_arrive = 0ull;
         h->cg_gamma = 0.0;
     }
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
@@ -901,11 +910,31 @@ int kpl_solver_iterate_persistent(const kpl_op *op, const kpl_cfg *cfgp, const k
             body.schedule = c.cfg.schedule; body.want_xi = 0; body.mout = nullptr;
             body.alpha = 0.0; body.beta = 0.0; body.asig = 0.0; body.wout = v->w1;
             void *args[] = {&g, const_cast<Layout *>(&L), &in_w, &body, &in_x, &tb,
-                            const_cast<Ws *>(&c.ws), const_cast<Cfg *>(&c.cfg), &first, &count};
+                            const_cast<Ws *>(&c.ws), const_cast<Cfg *>(&c.cfg), &first, &count, nullptr};
             int nb = 0, dev = 0;
             cudaGetDevice(&dev);
             int sms = kSMs;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            // redundant epilogue (one barrier per pass) when chunks are <= 32 items
+            // and the chunk table fits in shared memory; KPL_PERSIST_INLINE=1 forces
+            // the inline (counter-based) epilogue
+            const char *env = std::getenv("KPL_PERSIST_INLINE");
+            const size_t dsm = sizeof(double) * NQ * (size_t)(L.items + L.nch);   // item + chunk tables
+            if (L.T <= 32 && dsm <= 64 * 1024 && !(env && env[0] == '1')) {
+                char *ph = static_cast<char *>(workspace) + offsets(op, L, c.cfg.max_iters).pheads;
+                args[10] = &ph;
+                auto launch_red = [&](auto kern) -> int {
+                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, dsm);
+                    const long long cap = std::min((long long)nb * sms, kPersistMaxCtas);
+                    const unsigned grid = (unsigned)std::max(1LL, std::min(L.items, cap));
+                    g_launches.fetch_add(1, std::memory_order_relaxed);
+                    cudaLaunchCooperativeKernel((void *)kern, grid, NT, args, dsm, c.st);
+                    return cuda_check("persistent launch");
+                };
+                if (L.vx == 2) return launch_red(persistent_redundant<2, decltype(in_w), B, decltype(in_x)>);
+                return launch_red(persistent_redundant<1, decltype(in_w), B, decltype(in_x)>);
+            }
             if (L.vx == 2) {
                 auto kern = persistent_pipelined<2, decltype(in_w), B, decltype(in_x)>;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, 0);

@@ -29,7 +29,8 @@ struct WsHead {
     long long rr_held, rr_started;
     double cg_gamma, cg_beta, cg_rnorm, cg_alpha; // classic CG head -> delta
     long long cg_last, _cg_pad;
-    double dsig_pad[4];
+    unsigned long long bar_arrive;                // one-phase grid barrier (persistent_redundant)
+    double dsig_pad[3];
     unsigned int final_cnt, bar_cnt, bar_gen, _cnt_pad[5];   // completion count; grid barrier
 };
 static_assert(sizeof(WsHead) <= 1024, "head too large");
@@ -80,6 +81,7 @@ struct Ws {                   // device view of the caller's workspace
     int inline_final;         // 1: last CTA finalises (single GPU)
     double *prod;             // KPL_ORDER_BLOCKED8: products [NQ][nprod] for blocked_final_kernel
     long long nprod;
+    int hist_scratch;         // 1: history writes go to the single scratch row `hist` (redundant epilogues)
 };
 
 // Product sink of the reference-order mode: bodies accumulate through accp(),
@@ -183,14 +185,15 @@ __device__ __forceinline__ void block_sum(double (&v)[Q], double *sm /* >= NWARP
 // Levels 3/4: sum src[j*stride + q] for j in [0, count) -- thread t adds
 // j = t, t+256, ... sequentially from +0.0, then block_sum.  Loads bypass L1
 // (the values were written by other CTAs of this grid).
-template <int Q>
+template <int Q, bool SHARED = false>
 __device__ __forceinline__ void strided_sum(const double *src, long long count, int stride,
                                             double (&v)[Q], double *sm) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) v[q] = 0.0;
     for (long long j = threadIdx.x; j < count && threadIdx.x < NT; j += NT) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q) v[q] = __dadd_rn(v[q], __ldcg(src + j * stride + q));
+        for (int q = 0; q < Q; ++q)
+            v[q] = __dadd_rn(v[q], SHARED ? src[j * stride + q] : __ldcg(src + j * stride + q));
     }
     block_sum<Q>(v, sm);
 }
@@ -244,7 +247,9 @@ __device__ bool pipelined_scalars(WsHead *h, long long i, double gamma, double d
     return true;
 }
 
-__device__ __forceinline__ double *hist_row(const Ws &ws, long long i) { return ws.hist + HC * i; }
+__device__ __forceinline__ double *hist_row(const Ws &ws, long long i) {
+    return ws.hist_scratch ? ws.hist : ws.hist + HC * i;
+}
 
 __device__ __forceinline__ bool converged_test(const Cfg &cfg, const WsHead *h, double rnorm) {
     // solvers.py:391

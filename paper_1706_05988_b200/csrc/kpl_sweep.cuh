@@ -43,7 +43,7 @@ constexpr int CSR_WIN = 2048;      // staged nonzeros per window
 // one-launch-per-sweep kernel below and from the persistent solver kernel.
 // `spbuf` (2 * SMEM_PLANE doubles) and `sred` (NQ * NWARP) are the caller's
 // shared memory, so several passes in one kernel share it.
-template <int VX, class In, class Body>
+template <int VX, class In, class Body, bool FOLD = true>
 __device__ __forceinline__ void stencil_pass(const SGeo &g, const Layout &L, In in, Body body, const Ws &ws,
                                              const Cfg &cfg, int phase, double *spbuf, double *sred) {
     constexpr int Q = Body::NQ;
@@ -210,7 +210,7 @@ __device__ __forceinline__ void stencil_pass(const SGeo &g, const Layout &L, In 
 #pragma unroll
             for (int q = 0; q < Q; ++q) ws.items[item * NQ + q] = t[q];
         }
-        complete_item<Q>(ws, cfg, L, phase, c, sred);
+        if constexpr (FOLD) complete_item<Q>(ws, cfg, L, phase, c, sred);
     }
     __syncthreads();           // smem planes are restaged by the next item
     }
@@ -267,6 +267,123 @@ persistent_pipelined(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue
         }
         stencil_pass<VX, InW, BodyIt>(g, L, in_w, body, ws, cfg, PH_PIPE, sp, sred);
         grid_sync(ws.head);
+    }
+}
+
+// One-phase grid barrier: a monotone 64-bit arrival counter; barrier k of a
+// launch completes when the counter reaches base + k*grid.  One release
+// atomic to arrive, relaxed polling (an acquire load per poll would also
+// invalidate L1), one acquire load to leave.  `base` is the counter at
+// launch, rounded down to a multiple of the grid (every completed barrier
+// adds exactly one grid, and fewer than a grid of arrivals can precede any
+// CTA's first read).
+struct GridBarrier {
+    unsigned long long *cnt;
+    unsigned long long target;
+    __device__ void init(unsigned long long *c) {
+        cnt = c;
+        if (threadIdx.x == 0) {
+            unsigned long long v;
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+            target = v - v % gridDim.x;
+        }
+    }
+    __device__ void sync() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            target += gridDim.x;
+            unsigned long long v;
+            asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(v) : "l"(cnt) : "memory");
+            while (v < target) {
+                asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+            }
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+        }
+        __syncthreads();
+    }
+};
+
+// Redundant epilogue (small problems): after one grid barrier every CTA folds
+// all item partials itself -- level 3 one warp per chunk (chunks of <= 32
+// items: the block tree of complete_item reduces to warp 0's butterfly, the
+// other warps adding +0.0, which is exact because no partial of the form
+// 0.0 + x is -0.0), level 4 the same strided tree over the chunk values in
+// shared memory -- and runs the scalar epilogue on its own copy of the head.
+// Every CTA therefore holds the same alpha, beta, state as the inline path
+// without the chunk/final counter round trips or a second barrier.
+template <int Q>
+__device__ void fold_redundant(const Ws &wl, const Cfg &cfg, const Layout &L, int phase, double *sitems,
+                               double *schunk, double *sred) {
+    // one parallel, coalesced copy of the item table (a single L2 round trip)
+    const long long nitem = L.items * NQ;
+    for (long long k = threadIdx.x; k < nitem; k += blockDim.x) sitems[k] = __ldcg(wl.items + k);
+    __syncthreads();
+    // level 3, packed: with P = pow2 >= T, lanes [gP, gP+P) hold chunk g of the
+    // warp's group; the butterfly restricted to offsets < P gives lane gP exactly
+    // lane 0's value of the full 32-lane butterfly (the lanes >= P only add +0.0)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int P = 1;
+    while (P < L.T) P <<= 1;
+    const int per = 32 / P, sub = lane / P, idx = lane - sub * P;
+    for (long long c0 = (long long)warp * per; c0 < L.nch; c0 += (long long)NWARP * per) {
+        const long long c = c0 + sub;
+        const long long i0 = c * L.T;
+        const int cnt = c < L.nch ? (int)min((long long)L.T, L.items - i0) : 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            double v = idx < cnt ? __dadd_rn(0.0, sitems[(i0 + idx) * NQ + q]) : 0.0;
+            for (int off = P >> 1; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+            if (idx == 0 && c < L.nch) schunk[c * NQ + q] = v;
+        }
+    }
+    __syncthreads();
+    double f[Q];
+    strided_sum<Q, true>(schunk, L.nch, NQ, f, sred);
+    if (threadIdx.x == 0) {
+        double full[NQ] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < Q; ++q) full[q] = f[q];
+        finalize(wl, cfg, phase, full);
+    }
+    __syncthreads();           // the CTA's head is read by every thread of the next pass
+}
+
+template <int VX, class InW, class BodyIt, class InX>
+__global__ void __launch_bounds__(NT, 2)
+persistent_redundant(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue tbody, Ws ws, Cfg cfg,
+                     long long first, long long count, char *pheads) {
+    __shared__ __align__(16) double sp[2 * SMEM_PLANE];
+    __shared__ double sred[NQ * NWARP];
+    extern __shared__ double sdyn[];                   // item table [items][NQ], chunk table [nch][NQ]
+    double *const sitems = sdyn, *const schunk = sdyn + NQ * L.items;
+    Ws wl = ws;
+    if (blockIdx.x > 0) {                              // private head + scratch history row
+        char *slot = pheads + (blockIdx.x - 1) * (1024 + 256);
+        WsHead *mine = reinterpret_cast<WsHead *>(slot);
+        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(ws.head);
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(mine);
+        for (int k = threadIdx.x; k < (int)(sizeof(WsHead) / 8); k += blockDim.x) dst[k] = __ldcg(src + k);
+        wl.head = mine;
+        wl.hist = reinterpret_cast<double *>(slot + 1024);
+        wl.hist_scratch = 1;
+        __syncthreads();
+    }
+    double *const items0 = ws.items, *const items1 = ws.items + NQ * L.items;
+    long long pass = 0;
+    GridBarrier bar;
+    bar.init(&ws.head->bar_arrive);
+    for (long long j = first; j < first + count; ++j) {
+        if (__ldcg(&wl.head->state) != KPL_ST_RUNNING) break;     // identical in every CTA
+        if (j % 10 == 0 && __ldcg(&wl.head->iter) == j) {         // true-residual cadence (row j)
+            wl.items = (pass++ & 1) ? items1 : items0;
+            stencil_pass<VX, InX, BodyTrue, false>(g, L, in_x, tbody, wl, cfg, PH_TRUE, sp, sred);
+            bar.sync();
+            fold_redundant<1>(wl, cfg, L, PH_TRUE, sitems, schunk, sred);
+        }
+        wl.items = (pass++ & 1) ? items1 : items0;
+        stencil_pass<VX, InW, BodyIt, false>(g, L, in_w, body, wl, cfg, PH_PIPE, sp, sred);
+        bar.sync();
+        fold_redundant<BodyIt::NQ>(wl, cfg, L, PH_PIPE, sitems, schunk, sred);
     }
 }
 

@@ -280,7 +280,9 @@ class _Solve:
         self.init()
         if callback is not None and self.cfg.method == "cg":
             return self._run_cg_callback(callback)
-        chunk = 1 if callback is not None else 8
+        # persistent launches stop on the device at convergence, so they can
+        # start with longer chunks (fewer status round trips)
+        chunk = 1 if callback is not None else (64 if self.persistent else 8)
         st = self.read_status()
         if callback is not None:
             self._callback(callback)

@@ -341,11 +341,17 @@ def test_var_shift_jacobi_csr_bitwise():
     assert same_bits(hist11(res), np.ascontiguousarray(ores.history)) and same_bits(res.x, ores.x)
 
 
+@pytest.mark.parametrize("inline", [False, True])
 @pytest.mark.parametrize("shape,jac,method", [((200, 200), False, "pcg_sh"), ((37, 23), False, "pcg"),
-                                              ((64, 48), True, "pcg_sh"), ((24, 20, 16), False, "pcg_var_sh")])
-def test_persistent_solver_bitwise(shape, jac, method):
-    """The persistent cooperative path (small stencils) == per-iteration launches, bit for bit."""
+                                              ((64, 48), True, "pcg_sh"), ((24, 20, 16), False, "pcg_var_sh"),
+                                              ((130, 20, 16), False, "pcg_sh"), ((320, 64, 4), True, "pcg")])
+def test_persistent_solver_bitwise(shape, jac, method, inline, monkeypatch):
+    """The persistent cooperative path (small stencils) == per-iteration launches, bit for bit,
+    with the redundant per-CTA epilogue (chunks of <= 32 items; (320, 64, 4) has 40 and
+    takes the inline path) and with the inline counter-based epilogue forced."""
     from paper_1706_05988_b200.solvers import _Solve
+    if inline:
+        monkeypatch.setenv("KPL_PERSIST_INLINE", "1")
     A = K.Stencil2D(*shape) if len(shape) == 2 else K.Stencil3D(*shape)
     M = K.make_jacobi(A) if jac else None
     b = np.random.default_rng(4).normal(size=A.n)
