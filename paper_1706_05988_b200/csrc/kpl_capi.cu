@@ -265,7 +265,13 @@ int with_pc(const kpl_op *op, F &&f) {
 }
 
 // ------------------------------------------------------------ TMA path
-constexpr int kTmaDepth = 2;
+#ifndef KPL_TMA_DEPTH
+#define KPL_TMA_DEPTH 2
+#endif
+#ifndef KPL_TMA_DEPTH8_2D
+#define KPL_TMA_DEPTH8_2D 2
+#endif
+constexpr int kTmaDepth = KPL_TMA_DEPTH;
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
@@ -274,15 +280,17 @@ std::once_flag g_encode_once;
 // the 8-stream Jacobi update (86 KB, 2 CTAs/SM)
 template <class Body>
 constexpr int tma_depth() { return Body::kTmaStreams > 5 ? 1 : kTmaDepth; }
+template <class Body, bool TWO_D>
+constexpr int tma_depth2() { return (TWO_D && Body::kTmaStreams > 5) ? KPL_TMA_DEPTH8_2D : tma_depth<Body>(); }
 
 template <class Body, int PCIN = 0>
 void tma_prepare() {
-    cudaFuncSetAttribute(tma_sweep<Body, tma_depth<Body>(), PCIN, false>,
+    cudaFuncSetAttribute(tma_sweep<Body, tma_depth2<Body, false>(), PCIN, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TmaRing<tma_depth<Body>(), Body::kTmaStreams, false>::bytes());
-    cudaFuncSetAttribute(tma_sweep<Body, tma_depth<Body>(), PCIN, true>,
+                         (int)TmaRing<tma_depth2<Body, false>(), Body::kTmaStreams, false>::bytes());
+    cudaFuncSetAttribute(tma_sweep<Body, tma_depth2<Body, true>(), PCIN, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TmaRing<tma_depth<Body>(), Body::kTmaStreams, true>::bytes());
+                         (int)TmaRing<tma_depth2<Body, true>(), Body::kTmaStreams, true>::bytes());
     cudaGetLastError();
 }
 
@@ -337,7 +345,7 @@ int launch_tma(const kpl_op *op, const Layout &L, const double *in0, const doubl
                const double *const *streams, const Body &body, const Ws &ws, const Cfg &cfg, int phase,
                int pred, long long row, cudaStream_t st) {
     constexpr int NSTR = Body::kTmaStreams;
-    constexpr int DEPTH = tma_depth<Body>();
+    constexpr int DEPTH = tma_depth2<Body, false>(), DEPTH2 = tma_depth2<Body, true>();
     TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     const int zext = op->zhalo ? 1 : 0;
@@ -352,7 +360,7 @@ int launch_tma(const kpl_op *op, const Layout &L, const double *in0, const doubl
     SGeo g{op->nx, op->ny, op->nz, op->diag, nullptr, nullptr, op->zhalo};
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (two_d)
-        tma_sweep<Body, DEPTH, PCIN, true><<<(unsigned)L.items, NT + 32, TmaRing<DEPTH, NSTR, true>::bytes(), st>>>(
+        tma_sweep<Body, DEPTH2, PCIN, true><<<(unsigned)L.items, NT + 32, TmaRing<DEPTH2, NSTR, true>::bytes(), st>>>(
             maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext, op->pc_const);
     else
         tma_sweep<Body, DEPTH, PCIN, false><<<(unsigned)L.items, NT + 32, TmaRing<DEPTH, NSTR, false>::bytes(),

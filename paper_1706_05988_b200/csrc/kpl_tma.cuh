@@ -13,8 +13,9 @@
 //     expect_tx + TMA 5 stream boxes (64x8)   9 recurrences, stores to HBM (st.global.cs)
 //                                             arrive empty[...] (slot free)
 //
-// The w ring holds SW = D+3 planes (stencil needs z-1..z+1, D planes ahead);
-// the stream ring SS = D+1 stages.  Dirichlet ghosts (x,y,z out of range) are
+// The w ring holds SW = D+2 planes (the stencil needs z-1..z+1; a freed
+// plane is refilled one step ahead); the stream ring SS = D+1 stages.  Two
+// producer lanes (w ring, stream ring) run independently.  Dirichlet ghosts (x,y,z out of range) are
 // the TMA out-of-bounds zero fill, so the consumer has no boundary logic.
 // With D = 2 and the 5 streams of the p-CG-sh update: 5 x 5.4 KB + 3 x 20 KB
 // ~ 89 KB smem per CTA, 2 CTAs per SM,
@@ -85,9 +86,13 @@ __device__ __forceinline__ void tma_load3d(void *dst, const CUtensorMap *map, in
         : "memory");
 }
 
+#ifndef KPL_TMA_WEXTRA
+#define KPL_TMA_WEXTRA 2
+#endif
 template <int D, int NSTR, bool TWO_D = false>
 struct TmaRing {
-    static constexpr int SW = D + 3, SS = D + 1;
+    // w ring: the stencil's planes z-1..z+1 plus (WEXTRA - 1) ahead; streams D ahead
+    static constexpr int SW = D + KPL_TMA_WEXTRA, SS = D + 1;
     static constexpr size_t bytes() {
         return (size_t)SW * TmaShape<TWO_D>::WPLANE * 8 + (size_t)SS * NSTR * TMA_SPLANE * 8 + 8 * 2 * (SW + SS);
     }
@@ -145,37 +150,36 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
     for (int q = 0; q < Q; ++q) acc[q][0] = acc[q][1] = 0.0;
 
     if (warp == NWARP) {
-        // ------------------------------------------------------ producer
+        // ------------------------------------------------------ producers
+        // lane 0 feeds the w ring, lane 1 the stream ring: each throttled only by
+        // its own ring's empty barriers, so neither waits behind the other
         if (lane == 0) {
             const CUtensorMap *wm = par ? &maps.w[1] : &maps.w[0];
-            int p = 0, q = 0;
-            while (p < nw || q < ns) {
-                if (p < nw && (p <= q + 2 || q >= ns)) {
-                    const int slot = p % SW;
-                    if (p >= SW) mbar_wait(&wempty[slot], ((p / SW) - 1) & 1);
-                    mbar_expect_tx(&wfull[slot], WBYTES);
-                    const int zc_ = z0 - 1 + p + wzoff;
-                    if constexpr (TWO_D) {
+            for (int p = 0; p < nw; ++p) {
+                const int slot = p % SW;
+                if (p >= SW) mbar_wait(&wempty[slot], ((p / SW) - 1) & 1);
+                mbar_expect_tx(&wfull[slot], WBYTES);
+                const int zc_ = z0 - 1 + p + wzoff;
+                if constexpr (TWO_D) {
 #pragma unroll
-                        for (int cpy = 0; cpy < S::WCOPIES; ++cpy)
-                            tma_load3d(wring + slot * TMA_WPLANE + cpy * S::WBX, wm, x0 - 2 + cpy * S::WBX, 0, zc_,
-                                       &wfull[slot]);
-                    } else {
-                        tma_load3d(wring + slot * TMA_WPLANE, wm, x0 - 2, y0 - 1, zc_, &wfull[slot]);
-                    }
-                    ++p;
+                    for (int cpy = 0; cpy < S::WCOPIES; ++cpy)
+                        tma_load3d(wring + slot * TMA_WPLANE + cpy * S::WBX, wm, x0 - 2 + cpy * S::WBX, 0, zc_,
+                                   &wfull[slot]);
                 } else {
-                    const int slot = q % SS;
-                    if (q >= SS) mbar_wait(&sempty[slot], ((q / SS) - 1) & 1);
-                    mbar_expect_tx(&sfull[slot], SBYTES);
-#pragma unroll
-                    for (int s = 0; s < NSTR; ++s)
-#pragma unroll
-                        for (int cpy = 0; cpy < S::SCOPIES; ++cpy)
-                            tma_load3d(sring + (slot * NSTR + s) * TMA_SPLANE + cpy * S::SBX, &maps.s[s],
-                                       x0 + cpy * S::SBX, y0, z0 + q, &sfull[slot]);
-                    ++q;
+                    tma_load3d(wring + slot * TMA_WPLANE, wm, x0 - 2, y0 - 1, zc_, &wfull[slot]);
                 }
+            }
+        } else if (lane == 1) {
+            for (int q = 0; q < ns; ++q) {
+                const int slot = q % SS;
+                if (q >= SS) mbar_wait(&sempty[slot], ((q / SS) - 1) & 1);
+                mbar_expect_tx(&sfull[slot], SBYTES);
+#pragma unroll
+                for (int s = 0; s < NSTR; ++s)
+#pragma unroll
+                    for (int cpy = 0; cpy < S::SCOPIES; ++cpy)
+                        tma_load3d(sring + (slot * NSTR + s) * TMA_SPLANE + cpy * S::SBX, &maps.s[s],
+                                   x0 + cpy * S::SBX, y0, z0 + q, &sfull[slot]);
             }
         }
     } else {
