@@ -37,7 +37,13 @@ struct CGeo {
 // Largest smem plane: 3D tile (1x8 warps, VX=2): 10 rows x (128+4); 2D tile
 // (8x1 warps, VX=2): 3 rows x (512+4).
 constexpr int SMEM_PLANE = 1548;
-constexpr int CSR_WIN = 2048;      // staged nonzeros per window
+#ifndef KPL_CSR_WIN
+#define KPL_CSR_WIN 1024
+#endif
+#ifndef KPL_SPMV_MINB
+#define KPL_SPMV_MINB 6
+#endif
+constexpr int CSR_WIN = KPL_CSR_WIN;   // staged nonzeros per window
 
 // One pass of a stencil sweep over all items (grid-stride), callable from the
 // one-launch-per-sweep kernel below and from the persistent solver kernel.
@@ -403,7 +409,7 @@ persistent_redundant(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue
 //                    chunk.  The item (256 rows) and chunk trees are the ones
 //                    oracle/gpu_order.py emulates.
 template <class In>
-__global__ void __launch_bounds__(NT, 6)
+__global__ void __launch_bounds__(NT, KPL_SPMV_MINB)
 csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
     constexpr int PER = CSR_WIN / NT;
     __shared__ double sprod[CSR_WIN];
