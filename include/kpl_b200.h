@@ -9,8 +9,9 @@
  * Conventions
  *  - Every pointer is a DEVICE pointer unless stated otherwise; sizes are
  *    element counts; `stream` is a cudaStream_t passed as void*.
- *  - The library never allocates or frees device memory.  Scratch space is a
- *    caller buffer of kpl_workspace_bytes() bytes (256-byte aligned).
+ *  - The library never allocates or frees device memory, except the
+ *    peer-shareable regions of kpl_ipc_alloc (multi-GPU).  Scratch space is
+ *    a caller buffer of kpl_workspace_bytes() bytes (256-byte aligned).
  *  - Return value: 0 = ok, < 0 = error (see KPL_E*); kpl_last_error()
  *    returns a static message for the most recent error on the calling thread.
  *  - All launches are asynchronous on `stream`; nothing synchronises except
@@ -277,6 +278,58 @@ int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfg, int32_t kind, int6
    the whole table (for ncclAllGather).                                      */
 int kpl_chunk_table(const kpl_op *op, void *workspace, void **local, void **global,
                     int64_t *local_bytes);
+
+/* ---- device-initiated exchange over peer memory (NVLink P2P) ----------
+   Replaces the host-driven NCCL halo send/recv + chunk-table all-gather of
+   the multi-GPU sweep sequence (the reference has no parallel layer; the
+   paper's runs used PETSc/MPI, PAPER.md:625-630 -- the communication the
+   p-CG-sh recurrences exist to hide).  Peer pointers come from
+   kpl_ipc_open (one process per GPU) or are plain device pointers when
+   several ranks share a device.  After each sweep, kpl_peer_post stores the
+   halo planes / ghost rows of the next sweep's stencil inputs and this
+   rank's chunk partials straight into the peers' memory and then publishes
+   `epoch` into every rank's flag word for this rank; kpl_peer_finalize waits
+   for every rank's flag and folds the gathered table (same tree as one GPU,
+   so results are bit-identical to the single-GPU solve).                 */
+#define KPL_PEER_MAX_COPIES 40
+#define KPL_PEER_MAX_RANKS  16
+
+typedef struct kpl_copy {
+    const double  *src;      /* local device vector                             */
+    const int32_t *idx;      /* NULL: dst[k] = src[k]; else dst[k] = src[idx[k]] */
+    double        *dst;      /* peer (or local) device pointer                  */
+    int64_t        count;
+} kpl_copy;
+
+typedef struct kpl_post {
+    int32_t   ncopies;                          /* <= KPL_PEER_MAX_COPIES          */
+    int32_t   nsignals;                         /* <= KPL_PEER_MAX_RANKS           */
+    kpl_copy  copies[KPL_PEER_MAX_COPIES];
+    uint64_t *signal[KPL_PEER_MAX_RANKS];       /* flag word of THIS rank in every
+                                                   rank's flag array (incl. own)  */
+    unsigned int *counter;                      /* local device word, initially 0,
+                                                   self-resetting                 */
+} kpl_post;
+
+/* Enqueue the copies of `post`, then (after a system-scope fence) store
+   `epoch` into every signal word.  Host-side `post` is passed by value.    */
+int kpl_peer_post(const kpl_post *post, uint64_t epoch, void *stream);
+/* Wait until flags[0..nranks) >= epoch (acquire, system scope; a 20 s
+   timeout turns the device status into BREAKDOWN with bd_code 7, "peer
+   exchange timeout"), then, for a reducing sweep `kind` (0 = wait only),
+   fold `table` (chunks_global x 4 doubles) and run the sweep's scalar
+   epilogue, as kpl_finalize_global does.                                  */
+int kpl_peer_finalize(const kpl_op *op, const kpl_cfg *cfg, int32_t kind, int64_t row, void *workspace,
+                      const double *table, const uint64_t *flags, int32_t nranks, uint64_t epoch,
+                      void *stream);
+/* Peer-shareable device memory (the one allocation the library makes):
+   cudaMalloc + zero fill + cudaIpcGetMemHandle; `handle64` receives the 64-byte
+   handle to send to the other ranks.  kpl_ipc_open maps a peer's handle
+   (cudaIpcMemLazyEnablePeerAccess).                                       */
+int kpl_ipc_alloc(int64_t bytes, void **ptr, void *handle64);
+int kpl_ipc_open(const void *handle64, void **ptr);
+int kpl_ipc_close(void *ptr);
+int kpl_ipc_free(void *ptr);
 
 #ifdef __cplusplus
 }

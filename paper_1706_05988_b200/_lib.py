@@ -60,6 +60,18 @@ class KplStatus(ctypes.Structure):
                 ("_pad", _i64 * 9)]
 
 
+KPL_PEER_MAX_COPIES, KPL_PEER_MAX_RANKS = 40, 16
+
+
+class KplCopy(ctypes.Structure):
+    _fields_ = [("src", _p), ("idx", _p), ("dst", _p), ("count", _i64)]
+
+
+class KplPost(ctypes.Structure):
+    _fields_ = [("ncopies", _i32), ("nsignals", _i32), ("copies", KplCopy * KPL_PEER_MAX_COPIES),
+                ("signal", _p * KPL_PEER_MAX_RANKS), ("counter", _p)]
+
+
 _SIGS = {
     "kpl_version": (_i32, []),
     "kpl_launch_count": (_i64, []),
@@ -94,6 +106,13 @@ _SIGS = {
     "kpl_ic0_levels": (_i32, [_i64, _p, _p, _i32, _p, _p, _p]),
     "kpl_ic0_factor": (_i32, [_i64, _p, _p, _p, _p, _d, _p, _p, ctypes.POINTER(_i64), _p]),
     "kpl_precond_apply": (_i32, [ctypes.POINTER(KplOp), _p, _p, _p, _p]),
+    "kpl_peer_post": (_i32, [ctypes.POINTER(KplPost), ctypes.c_uint64, _p]),
+    "kpl_peer_finalize": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), _i32, _i64, _p, _p, _p, _i32,
+                                 ctypes.c_uint64, _p]),
+    "kpl_ipc_alloc": (_i32, [_i64, ctypes.POINTER(_p), _p]),
+    "kpl_ipc_open": (_i32, [_p, ctypes.POINTER(_p)]),
+    "kpl_ipc_close": (_i32, [_p]),
+    "kpl_ipc_free": (_i32, [_p]),
     "kpl_chunk_table": (_i32, [ctypes.POINTER(KplOp), _p, ctypes.POINTER(_p), ctypes.POINTER(_p),
                                ctypes.POINTER(_i64)]),
 }

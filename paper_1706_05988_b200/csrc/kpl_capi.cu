@@ -20,6 +20,7 @@
 #include "kpl_sweep.cuh"
 #include "kpl_tma.cuh"
 #include "kpl_ic0.cuh"
+#include "kpl_peer.cuh"
 
 using namespace kpl;
 
@@ -432,6 +433,7 @@ const char *kpl_breakdown_message(int64_t code) {
     case BD_VANISH_DEN: return "vanishing alpha denominator";
     case BD_NONFINITE: return "non-finite coefficients";
     case BD_NONPOS_SP: return "nonpositive curvature (s, p)";
+    case BD_PEER_TIMEOUT: return "peer exchange timeout";
     default: return "";
     }
 }
@@ -1083,6 +1085,74 @@ int kpl_precond_apply(const kpl_op *op, const double *v, double *out, void *work
     default:
         return fail(KPL_EINVAL, "unknown preconditioner");
     }
+}
+
+int kpl_peer_post(const kpl_post *post, uint64_t epoch, void *stream) {
+    if (!post || !post->counter) return fail(KPL_EINVAL, "null post / counter");
+    if (post->ncopies < 0 || post->ncopies > KPL_PEER_MAX_COPIES) return fail(KPL_EINVAL, "too many copies");
+    if (post->nsignals < 0 || post->nsignals > KPL_PEER_MAX_RANKS) return fail(KPL_EINVAL, "too many signals");
+    long long most = 0;
+    for (int c = 0; c < post->ncopies; ++c) {
+        const kpl_copy &cp = post->copies[c];
+        if (cp.count < 0 || (cp.count && (!cp.src || !cp.dst))) return fail(KPL_EINVAL, "bad copy");
+        most = std::max(most, (long long)cp.count);
+    }
+    const unsigned grid = (unsigned)std::max(1LL, std::min(cdiv(most, NT), 2LL * kSMs));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    peer_post_kernel<<<grid, NT, 0, (cudaStream_t)stream>>>(*post, (unsigned long long)epoch);
+    return cuda_check("peer post");
+}
+
+int kpl_peer_finalize(const kpl_op *op, const kpl_cfg *cfgp, int32_t kind, int64_t row, void *workspace,
+                      const double *table, const uint64_t *flags, int32_t nranks, uint64_t epoch, void *stream) {
+    Layout L;
+    int rc = make_layout(op, L);
+    if (rc != KPL_OK) return rc;
+    if (!cfgp || !workspace || !flags) return fail(KPL_EINVAL, "null argument");
+    if (nranks < 1 || nranks > KPL_PEER_MAX_RANKS) return fail(KPL_EINVAL, "bad rank count");
+    int phase = PH_NONE, pred = PRED_ALWAYS;
+    if (kind != 0 && (rc = kind_phase(kind, phase, pred)) != KPL_OK) return rc;
+    if (phase != PH_NONE && !table) return fail(KPL_EINVAL, "reducing sweep needs the exchange table");
+    const Cfg cfg = make_cfg(cfgp);
+    Ws ws = make_ws(op, L, cfg.max_iters, workspace);
+    if (table) ws.chunks = const_cast<double *>(table);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    peer_finalize_kernel<<<1, NT, 0, (cudaStream_t)stream>>>(ws, cfg, phase, pred, row,
+                                                             reinterpret_cast<const unsigned long long *>(flags),
+                                                             nranks, (unsigned long long)epoch);
+    return cuda_check("peer finalize");
+}
+
+int kpl_ipc_alloc(int64_t bytes, void **ptr, void *handle64) {
+    if (bytes <= 0 || !ptr || !handle64) return fail(KPL_EINVAL, "bad argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    void *p = nullptr;
+    if (cudaMalloc(&p, (size_t)bytes) != cudaSuccess) return cuda_check("IPC region cudaMalloc");
+    if (cudaMemset(p, 0, (size_t)bytes) != cudaSuccess) { cudaFree(p); return cuda_check("IPC region memset"); }
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p) != cudaSuccess) { cudaFree(p); return cuda_check("cudaIpcGetMemHandle"); }
+    std::memcpy(handle64, &h, sizeof(h));
+    *ptr = p;
+    return KPL_OK;
+}
+
+int kpl_ipc_open(const void *handle64, void **ptr) {
+    if (!handle64 || !ptr) return fail(KPL_EINVAL, "bad argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    if (cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return cuda_check("cudaIpcOpenMemHandle");
+    return KPL_OK;
+}
+
+int kpl_ipc_close(void *ptr) {
+    if (cudaIpcCloseMemHandle(ptr) != cudaSuccess) return cuda_check("cudaIpcCloseMemHandle");
+    return KPL_OK;
+}
+
+int kpl_ipc_free(void *ptr) {
+    if (cudaFree(ptr) != cudaSuccess) return cuda_check("IPC region cudaFree");
+    return KPL_OK;
 }
 
 int kpl_chunk_table(const kpl_op *op, void *workspace, void **local, void **global, int64_t *local_bytes) {

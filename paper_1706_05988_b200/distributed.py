@@ -41,6 +41,7 @@ from . import _lib, device as D
 from .solvers import (HC, BreakdownError, SolveResult, SolverConfig, make_kcfg, records_from)
 
 _ZC_CHOICES = (16, 8, 4, 2, 1)
+_BD_PEER_TIMEOUT = 7          # kpl_breakdown_message(7) == "peer exchange timeout"
 
 
 class SlabPlan:
@@ -70,34 +71,82 @@ class SlabPlan:
         return slice(a, a + self.n_local)
 
 
+def storage_names(cfg, ident):
+    """State vectors a rank stores (identity aliases u=r, q=s, p=t share storage)."""
+    names = ["x", "r"]
+    if not ident:
+        names.append("u")
+    if cfg.method == "cg":
+        names += ["p", "p1", "s"]
+    else:
+        names += ["w0", "w1", "z", "s", "t"]
+        if not ident:
+            names += ["q", "p"]
+    return names
+
+
+_ALIGN = 256
+
+
+def _align(v):
+    return (v + _ALIGN - 1) // _ALIGN * _ALIGN
+
+
+class PeerLayout:
+    """Byte layout of one rank's peer-shareable region (device-initiated
+    exchange): flag words (one uint64 per rank, written by that rank's posts),
+    the post completion counter, the double-buffered exchange table
+    [2][chunks_global][4] fp64, then every stored state vector (interior +
+    halo planes / ghost rows).  Every rank computes every rank's layout."""
+
+    FLAGS = 0
+    COUNTER = 8 * _lib.KPL_PEER_MAX_RANKS
+
+    def __init__(self, names, n_total, chunks_global):
+        self.chunks_global = chunks_global
+        off = _align(self.COUNTER + 8)
+        self.table = off
+        off += _align(2 * 4 * 8 * chunks_global)
+        self.vec = {}
+        for nm in names:
+            self.vec[nm] = off
+            off += _align(8 * n_total)
+        self.bytes = off
+
+    def table_slot(self, parity):
+        return self.table + parity * 4 * 8 * self.chunks_global
+
+
 class _RankState:
     """Device state of one rank: vectors (interior + halo/ghost storage), op,
     kcfg, workspace and its chunk-table views.  Subclasses define the layout."""
 
     VEC_NAMES = ("x", "r", "u", "w0", "w1", "z", "q", "s", "t", "p", "p1")
 
-    def _alloc_vectors(self, cfg, ident, n, extra, device):
+    def _alloc_vectors(self, cfg, ident, n, extra, device, region=None, layout=None):
         """Every state vector as one tensor of n + extra values (extra = halo
-        or ghost storage); identity aliases u=r, q=s, p=t as on one GPU."""
+        or ghost storage); identity aliases u=r, q=s, p=t as on one GPU.
+        With a peer region (device-initiated exchange) the vectors are views
+        into it at the offsets of `layout`."""
         t = D.torch()
         f64 = dict(dtype=t.float64, device=device)
         self.full = {}
-        names = ["x", "r"]
-        if not ident:
-            names.append("u")
-        if cfg.method == "cg":
-            names += ["p", "p1", "s"]
-        else:
-            names += ["w0", "w1", "z", "s", "t"]
-            if not ident:
-                names += ["q", "p"]
+        names = storage_names(cfg, ident)
         for nm in names:
-            self.full[nm] = t.zeros(n + extra, **f64)
+            if region is None:
+                self.full[nm] = t.zeros(n + extra, **f64)
+            else:
+                o = layout.vec[nm]
+                self.full[nm] = region[o:o + 8 * (n + extra)].view(t.float64)
+                self.full[nm].zero_()
+        self.alias = {nm: nm for nm in names}
         if ident:
             self.full["u"] = self.full["r"]
+            self.alias["u"] = "r"
             if cfg.method != "cg":
                 self.full["q"] = self.full["s"]
                 self.full["p"] = self.full["t"]
+                self.alias["q"], self.alias["p"] = "s", "t"
         self.b = t.zeros(n, **f64)
 
     def _finish(self, op, cfg, kcfg, device, chunks_local):
@@ -152,11 +201,12 @@ class _RankState:
 class _SlabState(_RankState):
     """z-slab of a stencil grid: vectors carry one halo plane on each side."""
 
-    def __init__(self, plan: SlabPlan, rank, diag, pc_code, pc_const, cfg, device, kcfg):
+    def __init__(self, plan: SlabPlan, rank, diag, pc_code, pc_const, cfg, device, kcfg, region=None,
+                 layout=None):
         self.plan, self.rank, self.device = plan, rank, device
         self.ident = pc_code == _lib.KPL_PC_IDENTITY
         n, sxy = plan.n_local, plan.sxy
-        self._alloc_vectors(cfg, self.ident, n, 2 * sxy, device)
+        self._alloc_vectors(cfg, self.ident, n, 2 * sxy, device, region, layout)
         op = _lib.KplOp()
         op.kind = _lib.KPL_OP_STENCIL
         op.precond = pc_code
@@ -239,14 +289,14 @@ class RowPlan:
 class _RowState(_RankState):
     """Row block of a CSR matrix: vectors = [local rows | ghost values]."""
 
-    def __init__(self, plan: RowPlan, rank, A, M, pc_code, cfg, device, kcfg):
+    def __init__(self, plan: RowPlan, rank, A, M, pc_code, cfg, device, kcfg, region=None, layout=None):
         t = D.torch()
         self.plan, self.rank, self.device = plan, rank, device
         self.ident = pc_code == _lib.KPL_PC_IDENTITY
         info = plan.ranks[rank]
         n = info["r1"] - info["r0"]
         self.n_local, self.n_ghost = n, len(info["ghosts"])
-        self._alloc_vectors(cfg, self.ident, n, self.n_ghost, device)
+        self._alloc_vectors(cfg, self.ident, n, self.n_ghost, device, region, layout)
         up = lambda a, dt: t.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
         self.row_ptr = up(info["row_ptr"], np.int32)
         self.col_idx = up(info["col_idx"], np.int32)
@@ -409,6 +459,103 @@ class TorchComm:
             off += cq
 
 
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device bytes (wraps an IPC region
+    as a torch tensor without copying)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class _Regions:
+    """Peer-shareable regions of one layout set: this process's tensors, every
+    rank's base address, and the epoch counter of its flag words (flags are
+    never reset, so epochs keep increasing across the solves that reuse it)."""
+
+    def __init__(self, tensors, bases, owned=(), opened=()):
+        self.tensors, self.bases = tensors, bases
+        self.epoch = 0
+        self._owned, self._opened = list(owned), list(opened)
+
+    def close(self):
+        lib = _lib.load()
+        for p in self._opened:
+            lib.kpl_ipc_close(p)
+        for p in self._owned:
+            lib.kpl_ipc_free(p)
+        self._owned, self._opened, self.tensors = [], [], {}
+
+
+class LocalPeerComm(LocalComm):
+    """P ranks on one device exchanging through the device-initiated peer path
+    (kpl_peer_post / kpl_peer_finalize) with plain device pointers as the peer
+    pointers.  Every rank's sweep, post and finalize are launched in rank
+    order on one stream, so each wait is already satisfied when its kernel
+    starts (no kernel depends on another running concurrently)."""
+
+    peer = True
+
+    def __init__(self, P):
+        super().__init__(P)
+        self._cache = {}
+
+    def regions(self, sizes, device):
+        key = tuple(sizes)
+        if key not in self._cache:
+            t = D.torch()
+            tens = {q: t.zeros(sz, dtype=t.uint8, device=device) for q, sz in enumerate(sizes)}
+            self._cache = {key: _Regions(tens, [tens[q].data_ptr() for q in range(len(sizes))])}
+        return self._cache[key]
+
+
+class PeerComm(TorchComm):
+    """One process per GPU, exchanging through peer memory over NVLink: each
+    rank allocates its region with kpl_ipc_alloc, the 64-byte IPC handles are
+    all-gathered once through torch.distributed, and every rank maps the
+    others' regions (kpl_ipc_open).  Per sweep there is no host-side
+    collective: kpl_peer_post pushes halos + partials and signals,
+    kpl_peer_finalize waits and folds."""
+
+    peer = True
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        self._cache = {}
+
+    def regions(self, sizes, device):
+        key = tuple(sizes)
+        if key in self._cache:
+            return self._cache[key]
+        for r in self._cache.values():
+            r.close()
+        self._cache = {}
+        import ctypes
+        lib = _lib.load()
+        me, P = self.rank, self.size
+        ptr = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(64)
+        _lib.check(lib.kpl_ipc_alloc(int(sizes[me]), ctypes.byref(ptr), h), "IPC region")
+        handles = [None] * P
+        self.dist.all_gather_object(handles, bytes(h.raw), group=self.group)
+        bases, opened = [], []
+        for q in range(P):
+            if q == me:
+                bases.append(ptr.value)
+                continue
+            p = ctypes.c_void_p()
+            _lib.check(lib.kpl_ipc_open(ctypes.create_string_buffer(handles[q], 64), ctypes.byref(p)),
+                       f"IPC open of rank {q}")
+            bases.append(p.value)
+            opened.append(p.value)
+        t = D.torch()
+        tens = {me: t.as_tensor(_CudaArray(ptr.value, int(sizes[me])), device=device)}
+        self._cache[key] = _Regions(tens, bases, owned=[ptr.value], opened=opened)
+        # every rank has mapped every region before any rank pushes into one
+        self.dist.barrier(group=self.group)
+        return self._cache[key]
+
+
 class DistributedSolve:
     """Drive one partitioned solve (stencil z-slabs or CSR row blocks);
     `comm` decides which ranks are local."""
@@ -424,8 +571,11 @@ class DistributedSolve:
             pc = _lib.KPL_PC_IDENTITY if kind == "identity" else _lib.KPL_PC_JACOBI_VEC
             self.plan = RowPlan(A, comm.size, chunk_blocks)
             self.kcfg, self._keep = make_kcfg(cfg, A, self, self.device)
-            self.states = [_RowState(self.plan, r, A, M, pc, cfg, self.device, self.kcfg)
+            n_tot = [info["r1"] - info["r0"] + len(info["ghosts"]) for info in self.plan.ranks]
+            self._peer_regions(cfg, kind == "identity", n_tot)
+            self.states = [_RowState(self.plan, r, A, M, pc, cfg, self.device, self.kcfg, *self._region(r))
                            for r in comm.local_ranks()]
+            self._peer_ready()
             return
         NX, NY, NZ, diag = A.slab_spec() if hasattr(A, "slab_spec") else A.stencil_spec()
         self.plan = SlabPlan(NX, NY, NZ, comm.size, zc)
@@ -442,8 +592,115 @@ class DistributedSolve:
         else:
             raise NotImplementedError(f"preconditioner {kind!r} not on the device path")
         self.kcfg, self._keep = make_kcfg(cfg, A, self, self.device)
-        self.states = [_SlabState(self.plan, r, diag, pc, c, cfg, self.device, self.kcfg)
+        self._peer_regions(cfg, kind == "identity", [self.plan.n_local + 2 * self.plan.sxy] * comm.size)
+        self.states = [_SlabState(self.plan, r, diag, pc, c, cfg, self.device, self.kcfg, *self._region(r))
                        for r in comm.local_ranks()]
+        self._peer_ready()
+
+    # -- device-initiated exchange (peer comms)
+    def _peer_regions(self, cfg, ident, n_tot):
+        self.peer = bool(getattr(self.comm, "peer", False))
+        self._pending = None
+        if not self.peer:
+            return
+        if self.comm.size > _lib.KPL_PEER_MAX_RANKS:
+            raise ValueError(f"peer exchange supports up to {_lib.KPL_PEER_MAX_RANKS} ranks")
+        self._names = storage_names(cfg, ident)
+        self.layouts = [PeerLayout(self._names, n, self.plan.chunks_global) for n in n_tot]
+        self.reg = self.comm.regions([L.bytes for L in self.layouts], self.device)
+        self._posts = {}
+
+    def _region(self, r):
+        if not self.peer:
+            return (None, None)
+        return (self.reg.tensors[r], self.layouts[r])
+
+    def _peer_ready(self):
+        if self.peer:
+            self._dirty = set(self._names)
+
+    def _addr(self, q, name, elem_off=0):
+        """Device address of element `elem_off` of rank q's stored vector `name`."""
+        return self.reg.bases[q] + self.layouts[q].vec[name] + 8 * elem_off
+
+    def _halo_copies(self, s, name):
+        """(src, idx, dst, count) of the rows peers read of this rank's `name`."""
+        out = []
+        full = s.full[name].data_ptr()
+        if isinstance(s, _SlabState):
+            sxy, n = self.plan.sxy, self.plan.n_local
+            if s.rank > 0:                         # first plane -> rank-1's upper halo
+                out.append((full + 8 * sxy, None, self._addr(s.rank - 1, name, sxy + n), sxy))
+            if s.rank < self.comm.size - 1:        # last plane -> rank+1's lower halo
+                out.append((full + 8 * n, None, self._addr(s.rank + 1, name, 0), sxy))
+        else:
+            for q, idx in s.send_idx.items():      # packed rows -> q's ghost segment for this rank
+                info = self.plan.ranks[q]
+                off, cnt, _ = info["recv"][s.rank]
+                out.append((full, idx.data_ptr(), self._addr(q, name, info["r1"] - info["r0"] + off), cnt))
+        return out
+
+    def _post_struct(self, s, push, reducing, parity):
+        key = (s.rank, push, reducing, parity)
+        post = self._posts.get(key)
+        if post is not None:
+            return post
+        copies = []
+        for nm in push:
+            copies += self._halo_copies(s, nm)
+        P = self.comm.size
+        if reducing:                               # my chunk partials -> every rank's table slot
+            src = s.table_local.data_ptr()
+            for q in range(P):
+                dst = self.reg.bases[q] + self.layouts[q].table_slot(parity) + 32 * s.chunk_offset
+                copies.append((src, None, dst, 4 * s.chunks_local))
+        if len(copies) > _lib.KPL_PEER_MAX_COPIES:
+            raise ValueError(f"{len(copies)} peer copies exceed KPL_PEER_MAX_COPIES")
+        post = _lib.KplPost()
+        post.ncopies, post.nsignals = len(copies), P
+        for i, (src, idx, dst, cnt) in enumerate(copies):
+            c = post.copies[i]
+            c.src, c.idx, c.dst, c.count = src, idx, dst, cnt
+        for q in range(P):
+            post.signal[q] = self.reg.bases[q] + PeerLayout.FLAGS + 8 * s.rank
+        post.counter = self.reg.bases[s.rank] + PeerLayout.COUNTER
+        self._posts[key] = post
+        return post
+
+    def _flush(self, inputs=()):
+        """Issue the deferred post + finalize of the last sweep: push the halos
+        of `inputs` (the next sweep's stencil inputs) that changed since their
+        last push, this rank's chunk partials if the sweep reduces, signal,
+        then wait for every rank and fold."""
+        push = []
+        for nm in inputs:
+            st = self.states[0].alias[nm]
+            if st in self._dirty and st not in push:
+                push.append(st)
+        if self._pending is None and not push:
+            return
+        kind, row = self._pending if self._pending is not None else (0, 0)
+        lib = _lib.load()
+        reducing = kind != 0 and lib.kpl_sweep_phase(kind) != 0
+        self.reg.epoch += 1
+        e = self.reg.epoch
+        par = e & 1
+        hs = D.stream_handle()
+        for s in self.states:
+            _lib.check(lib.kpl_peer_post(self._post_struct(s, tuple(push), reducing, par), e, hs), "peer post")
+        for s in self.states:
+            L = self.layouts[s.rank]
+            table = self.reg.bases[s.rank] + L.table_slot(par)
+            _lib.check(lib.kpl_peer_finalize(s.op, s.kcfg, kind, row, D.ptr(s.ws), table,
+                                             self.reg.bases[s.rank] + PeerLayout.FLAGS, self.comm.size, e, hs),
+                       "peer finalize")
+        self._dirty.difference_update(push)
+        self._pending = None
+
+    def _status(self):
+        if self.peer:
+            self._flush()
+        return self.states[0].read_status()
 
     # -- collective building blocks
     def _all(self, fn):
@@ -454,6 +711,13 @@ class DistributedSolve:
         self.comm.exchange(self.states, name)
 
     def sweep(self, kind, row=0, inputs=()):
+        if self.peer:
+            self._flush(inputs)
+            self._all(lambda s: s.sweep(kind, row))
+            kept = {self.states[0].alias[nm] for nm in inputs}
+            self._dirty.update(nm for nm in self._names if nm not in kept)
+            self._pending = (kind, row)
+            return
         for nm in inputs:
             self.exchange(nm)
         self._all(lambda s: s.sweep(kind, row))
@@ -478,6 +742,8 @@ class DistributedSolve:
     def init(self):
         m = self.cfg.method
         self._all(lambda s: s.prepare())
+        if self.peer:
+            self._pending = (0, 0)    # barrier: no peer pushes into this rank before its prepare
         self.sweep(_lib.KPL_SW_BNORM)
         self.sweep(_lib.KPL_SW_INIT_R, inputs=("x",))
         if m != "cg":
@@ -516,24 +782,28 @@ class DistributedSolve:
 
     def run(self, poll=16):
         self.init()
-        st = self.states[0].read_status()
+        st = self._status()
         while st.state == _lib.KPL_ST_RUNNING and self.issued < self.limit:
             for _ in range(min(poll, self.limit - self.issued)):
                 self.step()
-            st = self.states[0].read_status()
+            st = self._status()
         return self.result()
 
     def result(self):
         s0 = self.states[0]
-        st = s0.read_status()
+        st = self._status()
         if st.state == _lib.KPL_ST_BREAKDOWN:
             msg = _lib.load().kpl_breakdown_message(st.bd_code).decode()
+            if st.bd_code == _BD_PEER_TIMEOUT:
+                raise _lib.KplError(f"multi-GPU exchange failed: {msg}")
             raise BreakdownError(int(st.bd_iter), msg)
         if st.state != _lib.KPL_ST_DONE:
             raise _lib.KplError(f"distributed solve ended in state {st.state}")
         rows = int(st.iter) + 1
         if np.isnan(s0.history(rows)[-1, 5]):
             self.record(int(st.iter), cadence_only=False)
+            if self.peer:
+                self._flush()
         history = records_from(s0.history(rows), rows)
         reps = []
         if st.n_replacements:

@@ -132,11 +132,15 @@ def _one_gpu(A, M, b, cfg, zc):
     return _Solve(A, M, b, None, cfg, zc=zc, slab_view=True).run()
 
 
+COMMS = ["LocalComm", "LocalPeerComm"]
+
+
 @gpu
+@pytest.mark.parametrize("comm", COMMS)
 @pytest.mark.parametrize("P", [2, 4])
 @pytest.mark.parametrize("method,extra", [("pcg_sh", {"shift": 2.30188679245283}), ("pcg", {}),
                                           ("cg", {}), ("pcg_rr", {})])
-def test_local_ranks_bitwise_3d(P, method, extra):
+def test_local_ranks_bitwise_3d(P, method, extra, comm):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_1706_05988_b200 as K
@@ -148,7 +152,7 @@ def test_local_ranks_bitwise_3d(P, method, extra):
     ref = _one_gpu(A, None, b, cfg, zc)
     plan = SlabPlan(64, 24, 32, P, zc)
     res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
-                            comm=LocalComm(P), zc=zc)
+                            comm=getattr(dmod, comm)(P), zc=zc)
     x = np.concatenate([xi.cpu().numpy() for xi in res.x])
     assert res.iterations == ref.iterations
     for a, c in zip(res.history, ref.history):
@@ -159,8 +163,9 @@ def test_local_ranks_bitwise_3d(P, method, extra):
 
 
 @gpu
+@pytest.mark.parametrize("comm", COMMS)
 @pytest.mark.parametrize("P", [2, 3])
-def test_local_ranks_bitwise_2d_jacobi(P):
+def test_local_ranks_bitwise_2d_jacobi(P, comm):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_1706_05988_b200 as K
@@ -173,7 +178,7 @@ def test_local_ranks_bitwise_2d_jacobi(P):
     ref = _one_gpu(A, M, b, cfg, zc)
     plan = SlabPlan(96, 1, 48, P, zc)
     res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
-                            comm=LocalComm(P), zc=zc)
+                            comm=getattr(dmod, comm)(P), zc=zc)
     x = np.concatenate([xi.cpu().numpy() for xi in res.x])
     assert res.iterations == ref.iterations and res.converged
     assert [r.alpha for r in res.history] == [r.alpha for r in ref.history]
@@ -181,9 +186,10 @@ def test_local_ranks_bitwise_2d_jacobi(P):
 
 
 @gpu
+@pytest.mark.parametrize("comm", COMMS)
 @pytest.mark.parametrize("method,extra", [("pcg_sh", {"shift": 1.0}),
                                           ("pcg_var_sh", {"shift_schedule": tuple(0.05 * k for k in range(41))})])
-def test_local_ranks_gaps_bitwise(method, extra):
+def test_local_ranks_gaps_bitwise(method, extra, comm):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_1706_05988_b200 as K
@@ -194,7 +200,7 @@ def test_local_ranks_gaps_bitwise(method, extra):
     ref = _one_gpu(A, None, b, cfg, 4)
     plan = SlabPlan(64, 16, 16, 2, 4)
     res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(2)], None, cfg,
-                            comm=LocalComm(2), zc=4)
+                            comm=getattr(dmod, comm)(2), zc=4)
     for a, c in zip(res.history, ref.history):
         assert (a.gap_f, a.gap_g, a.gap_h, a.gap_j, a.rnorm_true) == \
                (c.gap_f, c.gap_g, c.gap_h, c.gap_j, c.rnorm_true)
@@ -227,10 +233,11 @@ def test_row_plan_ghost_mapping_reproduces_global_spmv():
 
 
 @gpu
+@pytest.mark.parametrize("comm", COMMS)
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("method,extra", [("pcg_sh", {"shift": 0.4124626382901352}), ("cg", {}),
                                           ("pcg_rr", {})])
-def test_local_ranks_csr_bitwise(P, method, extra):
+def test_local_ranks_csr_bitwise(P, method, extra, comm):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_1706_05988_b200 as K
@@ -243,7 +250,7 @@ def test_local_ranks_csr_bitwise(P, method, extra):
     ref = K.solve(A, M, b, None, cfg)
     plan = RowPlan(A, P)
     res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
-                            comm=LocalComm(P))
+                            comm=getattr(dmod, comm)(P))
     x = np.concatenate([xi.cpu().numpy() for xi in res.x])
     assert res.iterations == ref.iterations and res.converged == ref.converged
     for a, c in zip(res.history, ref.history):
@@ -254,7 +261,8 @@ def test_local_ranks_csr_bitwise(P, method, extra):
 
 
 @gpu
-def test_local_ranks_csr_varcoef_identity_bitwise():
+@pytest.mark.parametrize("comm", COMMS)
+def test_local_ranks_csr_varcoef_identity_bitwise(comm):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_1706_05988_b200 as K
@@ -266,7 +274,7 @@ def test_local_ranks_csr_varcoef_identity_bitwise():
     ref = K.solve(A, None, b, None, cfg)
     plan = RowPlan(A, 2)
     res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(2)], None, cfg,
-                            comm=LocalComm(2))
+                            comm=getattr(dmod, comm)(2))
     for a, c in zip(res.history, ref.history):
         assert (a.alpha, a.gap_f, a.gap_g, a.gap_h, a.gap_j) == (c.alpha, c.gap_f, c.gap_g, c.gap_h, c.gap_j)
 
@@ -394,3 +402,162 @@ def test_multiprocess_gloo_on_one_gpu_bitwise(kind):
         assert its == ref.iterations
         assert alphas == [h.alpha for h in ref.history]
         assert xb == ref.x[plan.local_slice(r)].tobytes()
+
+
+# ------------------------------------------- device-initiated peer exchange
+
+def _host_execute_post(post, epoch):
+    """What peer_post_kernel does, on host memory: every copy, then the signals
+    (the addresses in `post` are CPU addresses when the regions are CPU tensors)."""
+    import ctypes
+    for i in range(post.ncopies):
+        c = post.copies[i]
+        n = int(c.count)
+        dst = np.frombuffer((ctypes.c_double * n).from_address(c.dst), dtype=np.float64)
+        if c.idx:
+            idx = np.frombuffer((ctypes.c_int32 * n).from_address(c.idx), dtype=np.int32)
+            m = int(idx.max()) + 1 if n else 0
+            src = np.frombuffer((ctypes.c_double * m).from_address(c.src), dtype=np.float64)
+            dst[:] = src[idx]
+        else:
+            dst[:] = np.frombuffer((ctypes.c_double * n).from_address(c.src), dtype=np.float64)
+    for q in range(post.nsignals):
+        ctypes.c_uint64.from_address(post.signal[q]).value = epoch
+
+
+def _cpu_peer_solve(monkeypatch, A, M, cfg, P, **kw):
+    from paper_1706_05988_b200 import device as Dv
+    monkeypatch.setattr(Dv, "require_cuda", lambda: torch.device("cpu"))
+    return dmod.DistributedSolve(A, M, cfg, dmod.LocalPeerComm(P), **kw)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_peer_post_plan_slab_cpu(monkeypatch, P):
+    """Peer-exchange plan of z-slabs (regions as CPU tensors, copies executed
+    on the host): halos = the neighbours' boundary planes (zero at the global
+    boundary), every rank's table slot = all ranks' partials in rank order,
+    every flag word = the epoch."""
+    import paper_1706_05988_b200 as K
+    NX, NY, NZ = 8, 5, 12
+    A = K.Stencil3D(NX, NY, NZ)
+    cfg = K.SolverConfig(method="pcg_sh", shift=1.0, max_iters=10)
+    S = _cpu_peer_solve(monkeypatch, A, None, cfg, P, zc=2)
+    g = np.arange(A.n, dtype=np.float64) + 0.5
+    for s in S.states:
+        s.interior("w1").copy_(torch.from_numpy(g[S.plan.local_slice(s.rank)]))
+        s.table_local.copy_(torch.arange(s.table_local.numel(), dtype=torch.float64) + 1000 * s.rank)
+    for s in S.states:
+        _host_execute_post(S._post_struct(s, ("w1",), True, 1), 7)
+    sxy, nzl = NX * NY, NZ // P
+    want_table = np.concatenate([np.arange(4 * S.plan.chunks_local) + 1000.0 * r for r in range(P)])
+    for s in S.states:
+        lo, first, last, hi = (v.numpy() for v in s.planes("w1"))
+        z0 = s.rank * nzl
+        assert lo.tobytes() == (g[(z0 - 1) * sxy:z0 * sxy] if s.rank else np.zeros(sxy)).tobytes()
+        z1 = z0 + nzl
+        assert hi.tobytes() == (g[z1 * sxy:(z1 + 1) * sxy] if s.rank < P - 1 else np.zeros(sxy)).tobytes()
+        reg = S.reg.tensors[s.rank]
+        L = S.layouts[s.rank]
+        slot = reg[L.table_slot(1):L.table_slot(1) + 32 * S.plan.chunks_global].view(torch.float64).numpy()
+        assert slot.tobytes() == want_table.tobytes()
+        flags = reg[:8 * P].view(torch.int64).numpy()
+        assert list(flags) == [7] * P
+        # the other slot and the other vectors are untouched
+        other = reg[L.table_slot(0):L.table_slot(0) + 32 * S.plan.chunks_global]
+        assert int(other.sum()) == 0
+        assert float(s.full["w0"].abs().sum()) == 0.0
+
+
+def test_peer_post_plan_rows_cpu(monkeypatch):
+    """Peer-exchange plan of CSR row blocks: every ghost value = the global
+    vector at that column, delivered by its owner's packed send list."""
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200 import problems
+    A = problems.banded_spd(12000, seed=0, band=1500)
+    M = K.make_jacobi(A)
+    cfg = K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=10)
+    P = 3
+    S = _cpu_peer_solve(monkeypatch, A, M, cfg, P, chunk_blocks=2)
+    g = np.arange(A.n, dtype=np.float64) * 0.25
+    for s in S.states:
+        s.interior("w0").copy_(torch.from_numpy(g[S.plan.local_slice(s.rank)]))
+        # CPU stand-ins for the int32 device send lists
+        s.send_idx = {q: v.to(torch.int32) for q, v in s.send_idx.items()}
+    S._posts.clear()
+    for s in S.states:
+        _host_execute_post(S._post_struct(s, ("w0",), False, 0), 3)
+    for s in S.states:
+        ghosts = s.full["w0"][s.n_local:].numpy()
+        assert ghosts.tobytes() == g[S.plan.ranks[s.rank]["ghosts"]].tobytes()
+        assert list(S.reg.tensors[s.rank][:8 * P].view(torch.int64).numpy()) == [3] * P
+
+
+def _ipc_post_worker(rank, world, port, q):
+    """One process of the IPC plumbing check: map the other rank's region
+    (cudaIpc on the same device), push halos + partials + signal with
+    kpl_peer_post, host barrier, then read this rank's region.  No kernel
+    waits on another process (the barrier orders them on the host)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1706_05988_b200 as K
+        from paper_1706_05988_b200 import _lib, device as Dv
+        torch.cuda.set_device(0)
+        NX, NY, NZ = 16, 6, 8
+        A = K.Stencil3D(NX, NY, NZ)
+        cfg = K.SolverConfig(method="pcg_sh", shift=1.0, max_iters=10)
+        S = dmod.DistributedSolve(A, None, cfg, dmod.PeerComm(), zc=2)
+        (s,) = S.states
+        g = torch.arange(A.n, dtype=torch.float64, device="cuda") + 0.5
+        s.interior("w0").copy_(g[S.plan.local_slice(rank)])
+        s.table_local.copy_(torch.arange(s.table_local.numel(), dtype=torch.float64) + 100 * rank)
+        torch.cuda.synchronize()
+        dist.barrier()
+        lib = _lib.load()
+        _lib.check(lib.kpl_peer_post(S._post_struct(s, ("w0",), True, 0), 5, Dv.stream_handle()), "post")
+        torch.cuda.synchronize()
+        dist.barrier()
+        sxy, nzl = NX * NY, NZ // world
+        lo, _, _, hi = s.planes("w0")
+        gh = g.cpu().numpy()
+        z0 = rank * nzl
+        ok_lo = lo.cpu().numpy().tobytes() == (gh[(z0 - 1) * sxy:z0 * sxy] if rank else np.zeros(sxy)).tobytes()
+        z1 = z0 + nzl
+        ok_hi = hi.cpu().numpy().tobytes() == (gh[z1 * sxy:(z1 + 1) * sxy] if rank < world - 1
+                                               else np.zeros(sxy)).tobytes()
+        L = S.layouts[rank]
+        reg = S.reg.tensors[rank]
+        slot = reg[L.table_slot(0):L.table_slot(0) + 32 * S.plan.chunks_global].view(torch.float64).cpu().numpy()
+        want = np.concatenate([np.arange(4 * S.plan.chunks_local) + 100.0 * r for r in range(world)])
+        flags = reg[:8 * world].view(torch.int64).cpu().numpy().tolist()
+        q.put((rank, ok_lo, ok_hi, slot.tobytes() == want.tobytes(), flags))
+        dist.barrier()
+        S.reg.close()
+    except Exception as exc:
+        q.put((rank, "error", repr(exc), None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+@gpu
+def test_ipc_peer_post_two_processes_one_gpu():
+    """PeerComm's IPC regions (kpl_ipc_alloc / kpl_ipc_open) and kpl_peer_post
+    across two real processes sharing cuda:0."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_ipc_post_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok_lo, ok_hi, ok_table, flags in res:
+        assert ok_lo != "error", ok_hi
+        assert ok_lo and ok_hi and ok_table, (rank, ok_lo, ok_hi, ok_table)
+        assert flags == [5, 5]
