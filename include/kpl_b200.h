@@ -311,6 +311,30 @@ typedef struct kpl_post {
                                                    self-resetting                 */
 } kpl_post;
 
+/* Fused form for the hot sweep (stencil z-slabs, KPL_SW_ITER): the sweep
+   itself stores its tile of the slab's boundary planes of the pushed outputs
+   into the neighbours' halos (read back from what each thread just wrote),
+   every chunk-completing CTA stores its chunk partial into every rank's
+   exchange-table slot `table_parity`, and the rank's last chunk signals
+   `epoch` -- so the exchange overlaps the sweep and no post kernel runs.
+   `px` is a DEVICE copy of this struct.  Follow with kpl_peer_finalize.   */
+#define KPL_PUSH_W 1     /* the ping-pong output w[wpar] (next sweep's input) */
+#define KPL_PUSH_X 2     /* x (next record's true-residual cadence input)      */
+
+typedef struct kpl_peer_sweep {
+    int32_t   nranks, _pad;
+    double   *table[2][KPL_PEER_MAX_RANKS];     /* every rank's table slot, by parity */
+    uint64_t *signal[KPL_PEER_MAX_RANKS];       /* as kpl_post.signal                 */
+    const double *w_src[2];                     /* local interiors of w0, w1          */
+    double   *w_lo[2], *w_hi[2];                /* neighbour halo planes (NULL at the
+                                                   global boundary)                  */
+    const double *x_src;
+    double   *x_lo, *x_hi;
+} kpl_peer_sweep;
+
+int kpl_sweep_peer(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, int32_t kind, int64_t row,
+                   void *workspace, const kpl_peer_sweep *px, uint64_t epoch, int32_t table_parity,
+                   int32_t push, int32_t wpar, void *stream);
 /* Enqueue the copies of `post`, then (after a system-scope fence) store
    `epoch` into every signal word.  Host-side `post` is passed by value.    */
 int kpl_peer_post(const kpl_post *post, uint64_t epoch, void *stream);

@@ -72,6 +72,15 @@ class KplPost(ctypes.Structure):
                 ("signal", _p * KPL_PEER_MAX_RANKS), ("counter", _p)]
 
 
+KPL_PUSH_W, KPL_PUSH_X = 1, 2
+
+
+class KplPeerSweep(ctypes.Structure):
+    _fields_ = [("nranks", _i32), ("_pad", _i32), ("table", (_p * KPL_PEER_MAX_RANKS) * 2),
+                ("signal", _p * KPL_PEER_MAX_RANKS), ("w_src", _p * 2), ("w_lo", _p * 2), ("w_hi", _p * 2),
+                ("x_src", _p), ("x_lo", _p), ("x_hi", _p)]
+
+
 _SIGS = {
     "kpl_version": (_i32, []),
     "kpl_launch_count": (_i64, []),
@@ -109,6 +118,8 @@ _SIGS = {
     "kpl_peer_post": (_i32, [ctypes.POINTER(KplPost), ctypes.c_uint64, _p]),
     "kpl_peer_finalize": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), _i32, _i64, _p, _p, _p, _i32,
                                  ctypes.c_uint64, _p]),
+    "kpl_sweep_peer": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), ctypes.POINTER(KplVecs), _i32,
+                              _i64, _p, _p, ctypes.c_uint64, _i32, _i32, _i32, _p]),
     "kpl_ipc_alloc": (_i32, [_i64, ctypes.POINTER(_p), _p]),
     "kpl_ipc_open": (_i32, [_p, ctypes.POINTER(_p)]),
     "kpl_ipc_close": (_i32, [_p]),
@@ -140,6 +151,8 @@ def load():
                 "(there is no CPU fallback)")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("KPL_LIB") and not hasattr(lib, name):
+                continue          # an alternative (older) library under test: bind what it has
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -18,12 +18,12 @@ namespace kpl {
 
 enum Sel : int { SEL_FIXED = 0, SEL_ITER = 1, SEL_ITER1 = 2 };
 
-// Scalars and the iteration counter are read through L2 (__ldcg): inside a
-// persistent kernel they were written by another CTA after a grid barrier.
+// Scalars and the iteration counter are read with ld_head (strong, GPU scope,
+// compiler-ordered): inside a persistent kernel they were written after a barrier.
 __device__ __forceinline__ const double *pick(const WsHead *h, int sel, const double *a0,
                                               const double *a1) {
     if (sel == SEL_FIXED) return a0;
-    const long long par = (__ldcg(&h->iter) + (sel == SEL_ITER1 ? 1 : 0)) & 1;
+    const long long par = (ld_head(&h->iter) + (sel == SEL_ITER1 ? 1 : 0)) & 1;
     return par ? a1 : a0;
 }
 
@@ -278,10 +278,10 @@ struct BodyPcgIter {
     }
     __device__ void setup(const Ws &ws) {
         sk.set(ws);
-        alpha = __ldcg(&ws.head->alpha);
-        beta = __ldcg(&ws.head->beta);
+        alpha = ld_head(&ws.head->alpha);
+        beta = ld_head(&ws.head->beta);
         if constexpr (VAR) {
-            const long long i = __ldcg(&ws.head->iter);
+            const long long i = ld_head(&ws.head->iter);
             const double sp = schedule[i];
             sigma = schedule[i + 1];                    // sigma_cur; also the next delta's shift
             dsig = __dsub_rn(sigma, sp);                // solvers.py:481

@@ -147,6 +147,9 @@ Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspa
     ws.prod = ordered(op) ? reinterpret_cast<double *>(base + o.prod) : nullptr;
     ws.nprod = op->n;
     ws.hist_scratch = 0;
+    ws.px = nullptr;
+    ws.epoch = 0;
+    ws.tpar = ws.push = ws.wpar = 0;
     return ws;
 }
 
@@ -434,6 +437,7 @@ const char *kpl_breakdown_message(int64_t code) {
     case BD_NONFINITE: return "non-finite coefficients";
     case BD_NONPOS_SP: return "nonpositive curvature (s, p)";
     case BD_PEER_TIMEOUT: return "peer exchange timeout";
+    case BD_BARRIER_TIMEOUT: return "device barrier timeout";
     default: return "";
     }
 }
@@ -842,6 +846,25 @@ int kpl_sweep(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int32_t 
     Ctx c;
     int rc = make_ctx(op, cfgp, v, workspace, stream, c);
     if (rc != KPL_OK) return rc;
+    return do_sweep(c, kind, row);
+}
+
+int kpl_sweep_peer(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int32_t kind, int64_t row,
+                   void *workspace, const kpl_peer_sweep *px, uint64_t epoch, int32_t table_parity, int32_t push,
+                   int32_t wpar, void *stream) {
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
+    if (rc != KPL_OK) return rc;
+    if (!px) return fail(KPL_EINVAL, "null peer descriptor");
+    if (op->kind != KPL_OP_STENCIL || kind != KPL_SW_ITER || op->chunks_global <= 0)
+        return fail(KPL_EUNSUPPORTED, "fused peer exchange: multi-GPU stencil iteration sweeps only");
+    if (table_parity < 0 || table_parity > 1 || wpar < 0 || wpar > 1 || (push & ~(KPL_PUSH_W | KPL_PUSH_X)))
+        return fail(KPL_EINVAL, "bad parity / push mask");
+    c.ws.px = px;
+    c.ws.epoch = (unsigned long long)epoch;
+    c.ws.tpar = table_parity;
+    c.ws.push = push;
+    c.ws.wpar = wpar;
     return do_sweep(c, kind, row);
 }
 

@@ -8,6 +8,7 @@
 // contraction is impossible even if the flag were dropped.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include "../../include/kpl_b200.h"
 
@@ -82,6 +83,12 @@ struct Ws {                   // device view of the caller's workspace
     double *prod;             // KPL_ORDER_BLOCKED8: products [NQ][nprod] for blocked_final_kernel
     long long nprod;
     int hist_scratch;         // 1: history writes go to the single scratch row `hist` (redundant epilogues)
+    // fused multi-GPU exchange (kpl_sweep_peer; px == nullptr otherwise)
+    const kpl_peer_sweep *px;
+    unsigned long long epoch; // value signalled to every rank when this rank's sweep is done
+    int tpar;                 // exchange-table slot the chunk partials go to
+    int push;                 // KPL_PUSH_* outputs whose boundary planes go to the neighbours
+    int wpar;                 // which ping-pong w is the output
 };
 
 // Product sink of the reference-order mode: bodies accumulate through accp(),
@@ -136,6 +143,21 @@ __device__ __forceinline__ void ld_ro(const double *p, long long k, double (&o)[
     } else {
         o[0] = __ldg(p + k);
     }
+}
+
+// Reads of the workspace head (state, iteration, alpha, beta ...): a strong
+// GPU-scope load whose asm carries a "memory" clobber, so the compiler keeps
+// it after the barrier / epilogue stores that precede it in program order
+// (__ldcg's asm has no clobber, so nothing but the barrier orders it).
+__device__ __forceinline__ long long ld_head(const long long *p) {
+    long long v;
+    asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_head(const double *p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // ------------------------------------------------------------ arithmetic
@@ -206,6 +228,7 @@ enum Breakdown : int {
     BD_VANISH_DEN = 4,       // "vanishing alpha denominator"
     BD_NONFINITE = 5,        // "non-finite coefficients"
     BD_NONPOS_SP = 6,        // "nonpositive curvature (s, p)"
+    BD_BARRIER_TIMEOUT = 8,  // "device barrier timeout" (persistent solver; 7 = peer exchange timeout)
 };
 
 __device__ __forceinline__ void set_breakdown(WsHead *h, long long i, int code) {
@@ -395,13 +418,65 @@ __device__ void finalize(const Ws &ws, const Cfg &cfg, int phase, const double (
 // Per-kernel uniform predicate.
 __device__ __forceinline__ bool pred_ok(const WsHead *h, int pred, long long row) {
     if (pred == PRED_ALWAYS) return true;          // (plain spmv launches carry no workspace)
-    const long long state = __ldcg(&h->state);
+    const long long state = ld_head(&h->state);
     switch (pred) {
     case PRED_RUNNING: return state == KPL_ST_RUNNING;
-    case PRED_FIRE: return state == KPL_ST_RUNNING && __ldcg(&h->fire) != 0;
-    case PRED_ROW: return __ldcg(&h->iter) == row && state != KPL_ST_BREAKDOWN;
+    case PRED_FIRE: return state == KPL_ST_RUNNING && ld_head(&h->fire) != 0;
+    case PRED_ROW: return ld_head(&h->iter) == row && state != KPL_ST_BREAKDOWN;
     default: return true;
     }
+}
+
+// ---------------------------------------------------- fused peer exchange
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void peer_signal_all(const Ws &ws) {
+    for (int p = 0; p < ws.px->nranks; ++p)
+        st_release_sys_u64(reinterpret_cast<unsigned long long *>(ws.px->signal[p]), ws.epoch);
+}
+
+// A predicated-off fused sweep still signals (the finalize skips its fold by
+// the same predicate), so the ranks' epochs stay in step.
+__device__ __forceinline__ void peer_signal_idle(const Ws &ws) {
+    if (ws.px && blockIdx.x == 0 && threadIdx.x == 0) {
+        __threadfence_system();
+        peer_signal_all(ws);
+    }
+}
+
+// Halo part of the fused exchange: CTAs of the slab's first / last chunk copy
+// their tile of plane 0 / NZ-1 of each pushed output into the neighbour's
+// halo plane.  Each thread re-reads the elements it has just stored itself
+// (program order), k0 = x + NX*y of its first element.  Ends with a CTA
+// barrier and a system-scope fence, before the chunk completion count.
+template <int V>
+__device__ __forceinline__ void peer_halo_push(const Ws &ws, long long c, long long nch, long long NZ,
+                                               long long sxy, long long k0, bool ok) {
+    if (!ws.px || !ws.push) return;
+    const bool first = c == 0, last = c == nch - 1;
+    if (!first && !last) return;
+    const kpl_peer_sweep *px = ws.px;
+    if (ok) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            if (!(ws.push & (1 << m))) continue;
+            const double *src = m == 0 ? px->w_src[ws.wpar] : px->x_src;
+            double *lo = m == 0 ? px->w_lo[ws.wpar] : px->x_lo;
+            double *hi = m == 0 ? px->w_hi[ws.wpar] : px->x_hi;
+            if (first && lo) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) lo[k0 + v] = src[k0 + v];
+            }
+            if (last && hi) {
+                const long long kz = (NZ - 1) * sxy + k0;
+#pragma unroll
+                for (int v = 0; v < V; ++v) hi[k0 + v] = src[kz + v];
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
 }
 
 // After a CTA has written its item partial (thread 0, before the call):
@@ -431,6 +506,22 @@ __device__ void complete_item(const Ws &ws, const Cfg &cfg, const Layout &L, int
 #pragma unroll
         for (int q = 0; q < Q; ++q) ws.chunks[cg * NQ + q] = v[q];
         ws.chunk_cnt[chunk_local] = 0u;
+        if (ws.px) {
+            // fused exchange: this chunk's partial into every rank's table slot;
+            // the rank's last chunk signals every rank
+            for (int p = 0; p < ws.px->nranks; ++p) {
+                double *dst = ws.px->table[ws.tpar][p] + cg * NQ;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) dst[q] = q < Q ? v[q] : 0.0;
+            }
+            __threadfence_system();
+            const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
+            if (prev == (unsigned)(L.nch - 1)) {
+                ws.head->final_cnt = 0u;
+                __threadfence_system();
+                peer_signal_all(ws);
+            }
+        }
     }
     if (!ws.inline_final) return;
     if (threadIdx.x == 0) {

@@ -203,6 +203,7 @@ __device__ __forceinline__ void stencil_pass(const SGeo &g, const Layout &L, In 
         }
         cur = nxt;
     }
+    if constexpr (FOLD) peer_halo_push<VX>(ws, c, L.nch, g.NZ, sxy, x + NX * y, ok);   // (never in persistent passes)
 
     if constexpr (Q > 0) {
         double t[Q];
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(NT, 2)
 stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
     __shared__ __align__(16) double sp[Body::kStencil ? 2 * SMEM_PLANE : 2];
     __shared__ double sred[NQ * NWARP];
-    if (!pred_ok(ws.head, pred, row)) return;
+    if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
     stencil_pass<VX, In, Body>(g, L, in, body, ws, cfg, phase, sp, sred);
 }
 
@@ -265,9 +266,9 @@ persistent_pipelined(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue
     __shared__ __align__(16) double sp[2 * SMEM_PLANE];
     __shared__ double sred[NQ * NWARP];
     for (long long j = first; j < first + count; ++j) {
-        if (__ldcg(&ws.head->state) != KPL_ST_RUNNING) break;     // uniform: read after a barrier
+        if (ld_head(&ws.head->state) != KPL_ST_RUNNING) break;    // uniform: read after a barrier
         if (j % 10 == 0) {                                           // true-residual cadence (row j)
-            if (__ldcg(&ws.head->iter) == j)
+            if (ld_head(&ws.head->iter) == j)
                 stencil_pass<VX, InX, BodyTrue>(g, L, in_x, tbody, ws, cfg, PH_TRUE, sp, sred);
             grid_sync(ws.head);
         }
@@ -294,18 +295,35 @@ struct GridBarrier {
             target = v - v % gridDim.x;
         }
     }
-    __device__ void sync() {
+    // false: the barrier did not complete within 3 s (a bug, never a wait a
+    // correct run needs): the real head is marked BREAKDOWN / "device barrier
+    // timeout" and the caller leaves the kernel instead of hanging the GPU
+    __device__ bool sync(WsHead *real) {
+        __shared__ int s_ok;
         __syncthreads();
         if (threadIdx.x == 0) {
             target += gridDim.x;
-            unsigned long long v;
+            unsigned long long v, t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
             asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(v) : "l"(cnt) : "memory");
-            while (v < target) {
+            int ok = 1;
+            for (unsigned spin = 1; v < target; ++spin) {
                 asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+                if ((spin & 1023) == 0) {                       // the clock only now and then
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    if (t - t0 > 3000000000ull) { ok = 0; break; }
+                }
+            }
+            if (!ok) {
+                real->bd_code = BD_BARRIER_TIMEOUT;
+                real->bd_iter = -1;
+                atomicExch(reinterpret_cast<unsigned long long *>(&real->state), (unsigned long long)KPL_ST_BREAKDOWN);
             }
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+            s_ok = ok;
         }
         __syncthreads();
+        return s_ok;
     }
 };
 
@@ -354,6 +372,20 @@ __device__ void fold_redundant(const Ws &wl, const Cfg &cfg, const Layout &L, in
     __syncthreads();           // the CTA's head is read by every thread of the next pass
 }
 
+// A CTA-private view of the workspace, built field by field.  (Copying the
+// by-value kernel parameter `Ws ws` into a local and then changing fields of
+// the copy was miscompiled: nvcc 12.9 forwarded some reads of the copy to the
+// parameter, so private-head CTAs read CTA 0's head and the shared item
+// buffer -- the intermittent divergence/hang of the redundant-epilogue solver.)
+__device__ __forceinline__ Ws ws_view(const Ws &ws, WsHead *head, double *hist, int scratch, double *items) {
+    Ws w;
+    w.head = head; w.items = items; w.chunks = ws.chunks; w.chunk_cnt = ws.chunk_cnt; w.hist = hist;
+    w.reps = ws.reps; w.nbuf = ws.nbuf; w.mbuf = ws.mbuf; w.chunk_offset = ws.chunk_offset;
+    w.chunks_global = ws.chunks_global; w.inline_final = ws.inline_final; w.prod = ws.prod; w.nprod = ws.nprod;
+    w.hist_scratch = scratch; w.px = nullptr; w.epoch = 0; w.tpar = 0; w.push = 0; w.wpar = 0;
+    return w;
+}
+
 template <int VX, class InW, class BodyIt, class InX>
 __global__ void __launch_bounds__(NT, 2)
 persistent_redundant(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue tbody, Ws ws, Cfg cfg,
@@ -362,33 +394,37 @@ persistent_redundant(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue
     __shared__ double sred[NQ * NWARP];
     extern __shared__ double sdyn[];                   // item table [items][NQ], chunk table [nch][NQ]
     double *const sitems = sdyn, *const schunk = sdyn + NQ * L.items;
-    Ws wl = ws;
+    WsHead *head = ws.head;
+    double *hist = ws.hist;
+    int scratch = 0;
     if (blockIdx.x > 0) {                              // private head + scratch history row
         char *slot = pheads + (blockIdx.x - 1) * (1024 + 256);
         WsHead *mine = reinterpret_cast<WsHead *>(slot);
         const unsigned long long *src = reinterpret_cast<const unsigned long long *>(ws.head);
         unsigned long long *dst = reinterpret_cast<unsigned long long *>(mine);
         for (int k = threadIdx.x; k < (int)(sizeof(WsHead) / 8); k += blockDim.x) dst[k] = __ldcg(src + k);
-        wl.head = mine;
-        wl.hist = reinterpret_cast<double *>(slot + 1024);
-        wl.hist_scratch = 1;
+        head = mine;
+        hist = reinterpret_cast<double *>(slot + 1024);
+        scratch = 1;
         __syncthreads();
     }
-    double *const items0 = ws.items, *const items1 = ws.items + NQ * L.items;
+    // two views, one per item buffer (passes alternate them)
+    const Ws w0 = ws_view(ws, head, hist, scratch, ws.items);
+    const Ws w1 = ws_view(ws, head, hist, scratch, ws.items + NQ * L.items);
     long long pass = 0;
     GridBarrier bar;
     bar.init(&ws.head->bar_arrive);
     for (long long j = first; j < first + count; ++j) {
-        if (__ldcg(&wl.head->state) != KPL_ST_RUNNING) break;     // identical in every CTA
-        if (j % 10 == 0 && __ldcg(&wl.head->iter) == j) {         // true-residual cadence (row j)
-            wl.items = (pass++ & 1) ? items1 : items0;
+        if (ld_head(&head->state) != KPL_ST_RUNNING) break;        // identical in every CTA
+        if (j % 10 == 0 && ld_head(&head->iter) == j) {             // true-residual cadence (row j)
+            const Ws &wl = (pass++ & 1) ? w1 : w0;
             stencil_pass<VX, InX, BodyTrue, false>(g, L, in_x, tbody, wl, cfg, PH_TRUE, sp, sred);
-            bar.sync();
+            if (!bar.sync(ws.head)) return;
             fold_redundant<1>(wl, cfg, L, PH_TRUE, sitems, schunk, sred);
         }
-        wl.items = (pass++ & 1) ? items1 : items0;
+        const Ws &wl = (pass++ & 1) ? w1 : w0;
         stencil_pass<VX, InW, BodyIt, false>(g, L, in_w, body, wl, cfg, PH_PIPE, sp, sred);
-        bar.sync();
+        if (!bar.sync(ws.head)) return;
         fold_redundant<BodyIt::NQ>(wl, cfg, L, PH_PIPE, sitems, schunk, sred);
     }
 }

@@ -123,7 +123,7 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
     unsigned long long *sempty = wempty + SW;
     __shared__ double sred[NQ * NWARP];
 
-    if (!pred_ok(ws.head, pred, row)) return;
+    if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
     body.setup(ws);
     const long long par = wsel ? (ws.head->iter & 1) : 0;    // w_in = w[iter & 1] (ping-pong) or fixed
 
@@ -241,6 +241,12 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
                 mbar_arrive(&sempty[k % SS]);
             }
         }
+    }
+    if (ws.px) {                                  // fused multi-GPU exchange (kpl_sweep_peer)
+        const int wy = TWO_D ? 0 : warp;
+        const int xl = (TWO_D ? warp * 64 : 0) + 2 * lane;
+        const bool own = warp < NWARP && (y0 + wy < g.NY) && (x0 + xl < g.NX);
+        peer_halo_push<2>(ws, c, L.nch, g.NZ, g.NX * g.NY, (long long)(x0 + xl) + g.NX * (y0 + wy), own);
     }
 
     if constexpr (Body::NQ > 0) {

@@ -35,6 +35,8 @@ track_gaps.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _lib, device as D
@@ -105,6 +107,8 @@ class PeerLayout:
     def __init__(self, names, n_total, chunks_global):
         self.chunks_global = chunks_global
         off = _align(self.COUNTER + 8)
+        self.px = off                       # device copy of kpl_peer_sweep (fused sweeps)
+        off += _align(ctypes.sizeof(_lib.KplPeerSweep))
         self.table = off
         off += _align(2 * 4 * 8 * chunks_global)
         self.vec = {}
@@ -475,7 +479,8 @@ class _Regions:
 
     def __init__(self, tensors, bases, owned=(), opened=()):
         self.tensors, self.bases = tensors, bases
-        self.epoch = 0
+        self.epoch = 0          # last signalled flag value
+        self.red = 0            # reductions exchanged (table slot = red & 1)
         self._owned, self._opened = list(owned), list(opened)
 
     def close(self):
@@ -487,6 +492,14 @@ class _Regions:
         self._owned, self._opened, self.tensors = [], [], {}
 
 
+class LocalPeerCommPostOnly:
+    """LocalPeerComm without the fused sweep exchange (every sweep is
+    followed by a kpl_peer_post kernel) -- the parity tests run both."""
+
+    def __new__(cls, P):
+        return LocalPeerComm(P, fused=False)
+
+
 class LocalPeerComm(LocalComm):
     """P ranks on one device exchanging through the device-initiated peer path
     (kpl_peer_post / kpl_peer_finalize) with plain device pointers as the peer
@@ -496,8 +509,9 @@ class LocalPeerComm(LocalComm):
 
     peer = True
 
-    def __init__(self, P):
+    def __init__(self, P, fused=True):
         super().__init__(P)
+        self.fused = fused
         self._cache = {}
 
     def regions(self, sizes, device):
@@ -519,8 +533,9 @@ class PeerComm(TorchComm):
 
     peer = True
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, fused=True):
         super().__init__(group)
+        self.fused = fused
         self._cache = {}
 
     def regions(self, sizes, device):
@@ -601,8 +616,12 @@ class DistributedSolve:
     def _peer_regions(self, cfg, ident, n_tot):
         self.peer = bool(getattr(self.comm, "peer", False))
         self._pending = None
+        self.fused = False
         if not self.peer:
             return
+        # fused exchange inside the iteration sweep: stencil slabs, pipelined methods
+        self.fused = (bool(getattr(self.comm, "fused", True)) and isinstance(self.plan, SlabPlan)
+                      and cfg.method != "cg")
         if self.comm.size > _lib.KPL_PEER_MAX_RANKS:
             raise ValueError(f"peer exchange supports up to {_lib.KPL_PEER_MAX_RANKS} ranks")
         self._names = storage_names(cfg, ident)
@@ -616,8 +635,39 @@ class DistributedSolve:
         return (self.reg.tensors[r], self.layouts[r])
 
     def _peer_ready(self):
-        if self.peer:
-            self._dirty = set(self._names)
+        if not self.peer:
+            return
+        self._dirty = set(self._names)
+        if self.fused:
+            t = D.torch()
+            for s in self.states:
+                px = self._peer_sweep_struct(s)
+                raw = t.frombuffer(bytearray(bytes(px)), dtype=t.uint8)
+                o = self.layouts[s.rank].px
+                self.reg.tensors[s.rank][o:o + len(raw)].copy_(raw)     # stream-ordered before any sweep
+
+    def _peer_sweep_struct(self, s):
+        """kpl_peer_sweep of rank s: every rank's table slots and flag word for
+        s, and the neighbour halo planes of w0, w1 and x."""
+        P, r = self.comm.size, s.rank
+        sxy, n = self.plan.sxy, self.plan.n_local
+        px = _lib.KplPeerSweep()
+        px.nranks = P
+        for par in (0, 1):
+            for q in range(P):
+                px.table[par][q] = self.reg.bases[q] + self.layouts[q].table_slot(par)
+        for q in range(P):
+            px.signal[q] = self.reg.bases[q] + PeerLayout.FLAGS + 8 * r
+
+        def halos(name):
+            lo = self._addr(r - 1, name, sxy + n) if r > 0 else None
+            hi = self._addr(r + 1, name, 0) if r < P - 1 else None
+            return s.interior(name).data_ptr(), lo, hi
+
+        for k, nm in enumerate(("w0", "w1")):
+            px.w_src[k], px.w_lo[k], px.w_hi[k] = halos(nm)
+        px.x_src, px.x_lo, px.x_hi = halos("x")
+        return px
 
     def _addr(self, q, name, elem_off=0):
         """Device address of element `elem_off` of rank q's stored vector `name`."""
@@ -679,15 +729,21 @@ class DistributedSolve:
                 push.append(st)
         if self._pending is None and not push:
             return
-        kind, row = self._pending if self._pending is not None else (0, 0)
+        kind, row, e, par = self._pending if self._pending is not None else (0, 0, None, 0)
         lib = _lib.load()
         reducing = kind != 0 and lib.kpl_sweep_phase(kind) != 0
-        self.reg.epoch += 1
-        e = self.reg.epoch
-        par = e & 1
         hs = D.stream_handle()
-        for s in self.states:
-            _lib.check(lib.kpl_peer_post(self._post_struct(s, tuple(push), reducing, par), e, hs), "peer post")
+        if e is None or push:
+            # a post kernel: the halos, plus the partials unless the sweep pushed them itself
+            partials = reducing and e is None
+            if partials:
+                self.reg.red += 1
+                par = self.reg.red & 1
+            self.reg.epoch += 1
+            e = self.reg.epoch
+            for s in self.states:
+                _lib.check(lib.kpl_peer_post(self._post_struct(s, tuple(push), partials, par), e, hs),
+                           "peer post")
         for s in self.states:
             L = self.layouts[s.rank]
             table = self.reg.bases[s.rank] + L.table_slot(par)
@@ -710,13 +766,31 @@ class DistributedSolve:
     def exchange(self, name):
         self.comm.exchange(self.states, name)
 
-    def sweep(self, kind, row=0, inputs=()):
+    def sweep(self, kind, row=0, inputs=(), push_x=False):
         if self.peer:
             self._flush(inputs)
-            self._all(lambda s: s.sweep(kind, row))
             kept = {self.states[0].alias[nm] for nm in inputs}
+            if self.fused and kind == _lib.KPL_SW_ITER:
+                # the sweep pushes its w output (and x for the next cadence record)
+                # and its partials itself, then signals
+                self.reg.red += 1
+                self.reg.epoch += 1
+                e, par = self.reg.epoch, self.reg.red & 1
+                wout = "w0" if inputs[0] == "w1" else "w1"
+                push = _lib.KPL_PUSH_W | (_lib.KPL_PUSH_X if push_x else 0)
+                lib, hs = _lib.load(), D.stream_handle()
+                for s in self.states:
+                    pxd = self.reg.bases[s.rank] + self.layouts[s.rank].px
+                    _lib.check(lib.kpl_sweep_peer(s.op, s.kcfg, s.vecs, kind, row, D.ptr(s.ws), pxd, e, par, push,
+                                                  1 if wout == "w1" else 0, hs), "fused sweep")
+                clean = {wout} | ({"x"} if push_x else set())
+                self._dirty.update(nm for nm in self._names if nm not in kept)
+                self._dirty.difference_update(clean)
+                self._pending = (kind, row, e, par)
+                return
+            self._all(lambda s: s.sweep(kind, row))
             self._dirty.update(nm for nm in self._names if nm not in kept)
-            self._pending = (kind, row)
+            self._pending = (kind, row, None, 0)
             return
         for nm in inputs:
             self.exchange(nm)
@@ -743,7 +817,7 @@ class DistributedSolve:
         m = self.cfg.method
         self._all(lambda s: s.prepare())
         if self.peer:
-            self._pending = (0, 0)    # barrier: no peer pushes into this rank before its prepare
+            self._pending = (0, 0, None, 0)    # barrier: no peer pushes into this rank before its prepare
         self.sweep(_lib.KPL_SW_BNORM)
         self.sweep(_lib.KPL_SW_INIT_R, inputs=("x",))
         if m != "cg":
@@ -760,7 +834,9 @@ class DistributedSolve:
             self.sweep(_lib.KPL_SW_CG_P, inputs=(par, "u"))
             self.sweep(_lib.KPL_SW_CG_X)
         else:
-            self.sweep(_lib.KPL_SW_ITER, inputs=("w1" if (j & 1) else "w0",))
+            # x goes to the neighbours with the sweep when the next record reads it
+            px = not self.cfg.track_gaps and (j + 1) % 10 == 0
+            self.sweep(_lib.KPL_SW_ITER, inputs=("w1" if (j & 1) else "w0",), push_x=px)
             if m == "pcg_rr":
                 self.sweep(_lib.KPL_SW_RR_R, inputs=("x",))
                 self.sweep(_lib.KPL_SW_RR_W, inputs=("u",))
@@ -794,7 +870,7 @@ class DistributedSolve:
         st = self._status()
         if st.state == _lib.KPL_ST_BREAKDOWN:
             msg = _lib.load().kpl_breakdown_message(st.bd_code).decode()
-            if st.bd_code == _BD_PEER_TIMEOUT:
+            if st.bd_code >= _BD_PEER_TIMEOUT:
                 raise _lib.KplError(f"multi-GPU exchange failed: {msg}")
             raise BreakdownError(int(st.bd_iter), msg)
         if st.state != _lib.KPL_ST_DONE:

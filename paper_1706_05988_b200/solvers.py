@@ -23,6 +23,7 @@ bit for bit.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -223,6 +224,8 @@ class _Solve:
         self.hist_off = lib.kpl_history_offset(self.op)
         self.reps_off = lib.kpl_replacements_offset(self.op, cfg.max_iters)
         self.status = _lib.KplStatus()
+        if persistent is None and os.environ.get("KPL_NO_PERSISTENT") == "1":
+            persistent = False
         if persistent is None:
             persistent = (self.dm.kind == _lib.KPL_OP_STENCIL and n <= self.PERSISTENT_MAX_N
                           and cfg.method in ("pcg", "pcg_sh", "pcg_var_sh") and not cfg.track_gaps
@@ -299,6 +302,8 @@ class _Solve:
     # -- results ---------------------------------------------------------
     def _raise_breakdown(self, st):
         msg = _lib.load().kpl_breakdown_message(st.bd_code).decode()
+        if st.bd_code >= 7:                      # device-side failure, not arithmetic breakdown
+            raise _lib.KplError(f"device solve failed: {msg}")
         raise BreakdownError(int(st.bd_iter), msg)
 
     def history_array(self, rows):

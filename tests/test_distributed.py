@@ -9,6 +9,7 @@ GPU (one device, P virtual ranks via LocalComm): a P-rank solve is bit-identical
 to the 1-GPU solve, for every method, 2D and 3D, identity and Jacobi.
 """
 
+import ctypes
 import math
 import os
 import socket
@@ -18,7 +19,7 @@ import pytest
 import torch
 
 from oracle import gpu_order
-from paper_1706_05988_b200 import distributed as dmod
+from paper_1706_05988_b200 import _lib, distributed as dmod
 from paper_1706_05988_b200.distributed import RowPlan, SlabPlan, TorchComm
 
 
@@ -132,7 +133,7 @@ def _one_gpu(A, M, b, cfg, zc):
     return _Solve(A, M, b, None, cfg, zc=zc, slab_view=True).run()
 
 
-COMMS = ["LocalComm", "LocalPeerComm"]
+COMMS = ["LocalComm", "LocalPeerComm", "LocalPeerCommPostOnly"]
 
 
 @gpu
@@ -561,3 +562,30 @@ def test_ipc_peer_post_two_processes_one_gpu():
         assert ok_lo != "error", ok_hi
         assert ok_lo and ok_hi and ok_table, (rank, ok_lo, ok_hi, ok_table)
         assert flags == [5, 5]
+
+
+def test_peer_sweep_struct_cpu(monkeypatch):
+    """The fused sweep's device descriptor: table slots and flag words of every
+    rank, and the neighbour halo planes of w0/w1/x (none at the global boundary)."""
+    import paper_1706_05988_b200 as K
+    A = K.Stencil3D(8, 4, 12)
+    cfg = K.SolverConfig(method="pcg_sh", shift=1.0, max_iters=10)
+    P = 3
+    S = _cpu_peer_solve(monkeypatch, A, None, cfg, P, zc=2)
+    assert S.fused
+    sxy, n = 32, 32 * 4
+    for s in S.states:
+        o = S.layouts[s.rank].px
+        raw = bytes(S.reg.tensors[s.rank][o:o + ctypes.sizeof(_lib.KplPeerSweep)].numpy())
+        px = _lib.KplPeerSweep.from_buffer_copy(raw)
+        assert px.nranks == P
+        for q in range(P):
+            assert px.signal[q] == S.reg.bases[q] + 8 * s.rank
+            for par in (0, 1):
+                assert px.table[par][q] == S.reg.bases[q] + S.layouts[q].table_slot(par)
+        for k, nm in enumerate(("w0", "w1")):
+            assert px.w_src[k] == s.interior(nm).data_ptr()
+            lo = None if s.rank == 0 else S.states[s.rank - 1].full[nm][sxy + n:].data_ptr()
+            hi = None if s.rank == P - 1 else S.states[s.rank + 1].full[nm].data_ptr()
+            assert (px.w_lo[k], px.w_hi[k]) == (lo, hi)
+        assert px.x_src == s.interior("x").data_ptr()

@@ -363,3 +363,25 @@ def test_persistent_solver_bitwise(shape, jac, method, inline, monkeypatch):
     r2 = _Solve(A, M, b, None, cfg, persistent=False).run()
     assert r1.iterations == r2.iterations
     assert same_bits(hist11(r1), hist11(r2)) and same_bits(r1.x, r2.x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", [(200, 200), (64, 24, 32)])
+def test_persistent_solver_repeatable(dims):
+    """Repeated persistent (grid-barrier) solves equal the per-iteration-launch
+    solve bit for bit every time (guards the CTA-private workspace views of
+    persistent_redundant: a miscompiled copy made CTAs diverge now and then)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200.solvers import _Solve
+    A = K.Stencil2D(*dims) if len(dims) == 2 else K.Stencil3D(*dims)
+    b = np.full(A.n, 1.0 / np.sqrt(A.n))
+    cfg = K.SolverConfig(method="pcg_sh", shift=4.0 if len(dims) == 2 else 2.3, max_iters=300, rtol=0.0)
+    ref = _Solve(A, None, b, None, cfg, persistent=False).run()
+    want = [(r.alpha, r.beta, r.rnorm_recursive, r.rnorm_true) for r in ref.history]
+    for _ in range(25):
+        res = _Solve(A, None, b, None, cfg, persistent=True).run()
+        assert [(r.alpha, r.beta, r.rnorm_recursive, r.rnorm_true) for r in res.history] == want
+        assert np.asarray(res.x).tobytes() == np.asarray(ref.x).tobytes()
