@@ -589,3 +589,131 @@ def test_peer_sweep_struct_cpu(monkeypatch):
             hi = None if s.rank == P - 1 else S.states[s.rank + 1].full[nm].data_ptr()
             assert (px.w_lo[k], px.w_hi[k]) == (lo, hi)
         assert px.x_src == s.interior("x").data_ptr()
+
+
+# Writes of each sweep kind (storage names before aliasing; kpl_capi.cu do_sweep):
+# ITER j writes w[(j+1)&1], CG_P j writes p[(j+1)&1]; RR_W is taken to write both w.
+def _writes(kind, j):
+    L = _lib
+    if kind == L.KPL_SW_INIT_R or kind == L.KPL_SW_RR_R:
+        return {"r", "u"}
+    if kind == L.KPL_SW_INIT_W:
+        return {"w0"}
+    if kind == L.KPL_SW_ITER:
+        return {"x", "r", "u", "z", "q", "s", "t", "p", "w1" if j % 2 == 0 else "w0"}
+    if kind == L.KPL_SW_CG_P:
+        return {"p1" if j % 2 == 0 else "p", "s"}
+    if kind == L.KPL_SW_CG_X:
+        return {"x", "r", "u"}
+    if kind == L.KPL_SW_RR_W:
+        return {"w0", "w1"}
+    if kind == L.KPL_SW_RR_S:
+        return {"s", "q"}
+    if kind == L.KPL_SW_RR_Z:
+        return {"z"}
+    return set()
+
+
+@pytest.mark.parametrize("method,extra,gaps,fused", [
+    ("pcg_sh", {"shift": 1.0}, False, True), ("pcg_sh", {"shift": 1.0}, False, False),
+    ("pcg_sh", {"shift": 1.0}, True, True), ("pcg", {}, False, True), ("pcg_rr", {}, False, True),
+    ("cg", {}, False, True), ("cg", {}, True, False)])
+@pytest.mark.parametrize("jacobi", [False, True])
+def test_peer_exchange_schedule_is_fresh_and_race_free(monkeypatch, method, extra, gaps, fused, jacobi):
+    """Replays the distributed driver's sweep / post / finalize sequence with a
+    recording stand-in for the device calls and checks, against the write sets
+    of every sweep kind: (1) every halo a sweep reads was pushed after the last
+    write of that vector; (2) no push issued during or after sweep s targets a
+    vector sweep s reads (a peer may still be running sweep s); (3) a finalize
+    (wait) separates every two sweeps."""
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200 import device as Dv
+    monkeypatch.setattr(Dv, "require_cuda", lambda: torch.device("cpu"))
+    A = K.Stencil3D(8, 4, 8)
+    M = K.make_jacobi(A) if jacobi else None
+    cfg = K.SolverConfig(method=method, max_iters=40, track_gaps=gaps, **extra)
+    comm = dmod.LocalPeerComm(2, fused=fused)
+    S = dmod.DistributedSolve(A, M, cfg, comm, zc=2)
+    ev = []
+    real = _lib.load()
+
+    class FakeLib:
+        def kpl_sweep_phase(self, kind):
+            return real.kpl_sweep_phase(kind)
+
+        def kpl_peer_post(self, post, e, hs):
+            return 0
+
+        def kpl_peer_finalize(self, *a):
+            ev.append(("fin",))
+            return 0
+
+        def kpl_sweep_peer(self, op, kcfg, vecs, kind, row, ws, pxd, e, par, push, wpar, hs):
+            if ws == D0[0]:
+                ev.append(("sweep",) + cur[0])
+            pushed = set()
+            if push & _lib.KPL_PUSH_W:
+                pushed.add("w1" if wpar else "w0")
+            if push & _lib.KPL_PUSH_X:
+                pushed.add("x")
+            if ws == D0[0]:
+                ev.append(("fused", kind, pushed))
+            return 0
+
+    monkeypatch.setattr(_lib, "load", lambda: FakeLib())
+    orig_post = dmod.DistributedSolve._post_struct
+
+    def rec_post(self, s, push, reducing, parity):
+        if s.rank == 0:
+            ev.append(("post", set(push)))
+        return orig_post(self, s, push, reducing, parity)
+
+    monkeypatch.setattr(dmod.DistributedSolve, "_post_struct", rec_post)
+    orig_sweep = dmod.DistributedSolve.sweep
+
+    cur = [None]
+    D0 = [S.states[0].ws.data_ptr()]
+
+    def rec_sweep(self, kind, row=0, inputs=(), push_x=False):
+        cur[0] = (kind, {self.states[0].alias[n] for n in inputs}, getattr(self, "issued", 0))
+        return orig_sweep(self, kind, row, inputs, push_x)
+
+    def rank_sweep(self, kind, row=0):
+        if self.rank == 0:
+            ev.append(("sweep",) + cur[0])
+
+    monkeypatch.setattr(dmod.DistributedSolve, "sweep", rec_sweep)
+    monkeypatch.setattr(dmod._RankState, "sweep", rank_sweep)
+    monkeypatch.setattr(dmod._RankState, "prepare", lambda self: None)
+    monkeypatch.setattr(Dv, "stream_handle", lambda: None)
+    S.init()
+    for _ in range(23):
+        S.step()
+    S._flush()
+    alias = S.states[0].alias
+    version = {n: 0 for n in S._names}
+    pushed = {n: 0 for n in S._names}
+    prev_inputs, since_fin = set(), True
+    last_kind = last_j = None
+    for e in ev:
+        if e[0] == "sweep":
+            _, kind, inputs, j = e
+            assert since_fin, f"two sweeps without a finalize between them ({kind})"
+            for n in inputs:
+                assert pushed[n] == version[n], f"sweep {kind} at step {j} reads a stale halo of {n}"
+            for n in _writes(kind, j):
+                version[alias.get(n, n)] += 1
+            prev_inputs, since_fin = inputs, False
+            last_kind, last_j = kind, j
+        elif e[0] == "fused":
+            _, kind, push = e
+            assert not (push & prev_inputs), f"fused push {push} overlaps the sweep's inputs"
+            for n in push:
+                pushed[n] = version[n]
+        elif e[0] == "post":
+            assert not (e[1] & prev_inputs), f"post {e[1]} overlaps the inputs of sweep {last_kind} at step {last_j}: {ev[max(0, ev.index(e) - 8):ev.index(e) + 1]}"
+            for n in e[1]:
+                pushed[n] = version[n]
+        elif e[0] == "fin":
+            since_fin = True
+    assert since_fin
