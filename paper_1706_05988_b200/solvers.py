@@ -175,8 +175,13 @@ class _Solve:
 
     # stencil problems up to this size run as persistent cooperative launches
     # (one launch per chunk of iterations, grid barriers instead of kernel
-    # boundaries): there the per-iteration launch latency, not HBM, dominates
-    PERSISTENT_MAX_N = 1 << 20
+    # boundaries): there the per-iteration launch latency, not HBM, dominates.
+    # Measured crossover (tools/small_time.py, us/iteration persistent vs
+    # launches): 2D 200^2 13.3/17.5, 300^2 18.1/26.3, 400^2 21.3/28.1, 600^2
+    # 38.7/24.0; 3D 64x24x32 11.1/12.6, 48^3 15.6/14.6, 64^3 23.2/19.7 -- the
+    # redundant per-CTA fold grows with the item count.
+    PERSISTENT_MAX_N = 1 << 16
+    PERSISTENT_MAX_N_2D = 1 << 18
 
     def __init__(self, A, M, b, x0, cfg: SolverConfig, *, zc=0, vx=0, chunk_blocks=0, slab_view=False,
                  persistent=None):
@@ -227,7 +232,8 @@ class _Solve:
         if persistent is None and os.environ.get("KPL_NO_PERSISTENT") == "1":
             persistent = False
         if persistent is None:
-            persistent = (self.dm.kind == _lib.KPL_OP_STENCIL and n <= self.PERSISTENT_MAX_N
+            lim = self.PERSISTENT_MAX_N_2D if self.op.ny == 1 else self.PERSISTENT_MAX_N
+            persistent = (self.dm.kind == _lib.KPL_OP_STENCIL and n <= lim
                           and cfg.method in ("pcg", "pcg_sh", "pcg_var_sh") and not cfg.track_gaps
                           and self.op.order == _lib.KPL_ORDER_TREE)
         self.persistent = bool(persistent)
