@@ -437,7 +437,7 @@ def run_reference(args):
         return
     O, A, b = _cpu_setup()
     steps = args.steps
-    warm = min(args.warmup, 1)
+    warm = args.warmup
     times = cpu_iterations(steps, O, A, b, warm=warm)
     per = sum(times) / len(times)
     value = 1.0 / per

@@ -492,14 +492,6 @@ class _Regions:
         self._owned, self._opened, self.tensors = [], [], {}
 
 
-class LocalPeerCommPostOnly:
-    """LocalPeerComm without the fused sweep exchange (every sweep is
-    followed by a kpl_peer_post kernel) -- the parity tests run both."""
-
-    def __new__(cls, P):
-        return LocalPeerComm(P, fused=False)
-
-
 class LocalPeerComm(LocalComm):
     """P ranks on one device exchanging through the device-initiated peer path
     (kpl_peer_post / kpl_peer_finalize) with plain device pointers as the peer
@@ -521,6 +513,12 @@ class LocalPeerComm(LocalComm):
             tens = {q: t.zeros(sz, dtype=t.uint8, device=device) for q, sz in enumerate(sizes)}
             self._cache = {key: _Regions(tens, [tens[q].data_ptr() for q in range(len(sizes))])}
         return self._cache[key]
+
+
+def LocalPeerCommPostOnly(P):
+    """LocalPeerComm without the fused sweep exchange (every sweep is followed
+    by a kpl_peer_post kernel) -- the parity tests run both forms."""
+    return LocalPeerComm(P, fused=False)
 
 
 class PeerComm(TorchComm):
