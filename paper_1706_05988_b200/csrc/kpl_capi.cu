@@ -205,6 +205,25 @@ Cfg make_cfg(const kpl_cfg *c) {
 // ------------------------------------------------------------ dispatch
 struct NoSpmvIn {};
 
+// Launch with programmatic stream serialisation (PDL): the kernel's CTAs may be
+// scheduled while the previous kernel drains; the kernel itself starts with
+// griddepcontrol.wait.  KPL_PDL=0 launches normally.
+template <class Kern, class... Args>
+void launch_pdl(Kern kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st, Args... args) {
+    static const bool off = [] { const char *e = std::getenv("KPL_PDL"); return e && e[0] == '0'; }();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(block);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = off ? 0 : 1;
+    cudaLaunchKernelEx(&lc, kern, args...);
+}
+
 // `spin`: input of the CSR SpMV when it differs from the body's stencil input
 // (m = w * inv_diag materialised in the workspace); NoSpmvIn = use `in`.
 template <class In, class Body, class SpIn = NoSpmvIn>
@@ -219,9 +238,9 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
         SGeo g{op->nx, op->ny, op->nz, op->diag, op->halo_lo, op->halo_hi, op->zhalo};
         const unsigned grid = (unsigned)std::min(L.items, cap);
         if (L.vx == 2)
-            stencil_sweep<2, In, Body><<<grid, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
+            launch_pdl(stencil_sweep<2, In, Body>, grid, NT, 0, st, g, L, in, body, ws, cfg, phase, pred, row);
         else
-            stencil_sweep<1, In, Body><<<grid, NT, 0, st>>>(g, L, in, body, ws, cfg, phase, pred, row);
+            launch_pdl(stencil_sweep<1, In, Body>, grid, NT, 0, st, g, L, in, body, ws, cfg, phase, pred, row);
     } else {
         // split CSR: high-occupancy SpMV into the workspace, then the chunk sweep
         CGeo g{op->n, op->row_ptr, op->col_idx, op->values};
@@ -364,12 +383,13 @@ int launch_tma(const kpl_op *op, const Layout &L, const double *in0, const doubl
     SGeo g{op->nx, op->ny, op->nz, op->diag, nullptr, nullptr, op->zhalo};
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (two_d)
-        tma_sweep<Body, DEPTH2, PCIN, true><<<(unsigned)L.items, NT + 32, TmaRing<DEPTH2, NSTR, true>::bytes(), st>>>(
-            maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext, op->pc_const);
+        launch_pdl(tma_sweep<Body, DEPTH2, PCIN, true>, (unsigned)L.items, NT + 32,
+                   TmaRing<DEPTH2, NSTR, true>::bytes(), st, maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext,
+                   op->pc_const);
     else
-        tma_sweep<Body, DEPTH, PCIN, false><<<(unsigned)L.items, NT + 32, TmaRing<DEPTH, NSTR, false>::bytes(),
-                                              st>>>(maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext,
-                                                    op->pc_const);
+        launch_pdl(tma_sweep<Body, DEPTH, PCIN, false>, (unsigned)L.items, NT + 32,
+                   TmaRing<DEPTH, NSTR, false>::bytes(), st, maps, g, L, body, ws, cfg, phase, pred, row, wsel,
+                   zext, op->pc_const);
     return cuda_check("tma sweep launch");
 }
 

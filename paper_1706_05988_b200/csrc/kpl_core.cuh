@@ -160,6 +160,16 @@ __device__ __forceinline__ double ld_head(const double *p) {
     return v;
 }
 
+// Programmatic dependent launch: sweeps may be launched while the previous
+// kernel in the stream is still draining (cudaLaunchAttributeProgrammatic-
+// StreamSerialization); they wait here -- before touching anything the
+// previous kernel wrote -- and let their own dependents launch early.  Both
+// are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------ arithmetic
 // axpy(alpha, x, y) of sparse.py:172-180: alpha == 0 -> exact copy of y.
 __device__ __forceinline__ double axpy1(double a, double x, double y) {

@@ -45,9 +45,23 @@ __device__ __forceinline__ int ld_relaxed(const int *p) {
 // Spin with relaxed loads, then one acquire load: an acquire load also
 // invalidates the SM's L1 (CCTL.IVALL), so spinning on it would evict the
 // data every other warp on the SM is reading.
+// Watchdog of the dependency spins: a wait that a correct sweep satisfies in
+// microseconds; after ~10 s something is broken -- trap (the launch fails with
+// an error) rather than leave the GPU spinning.
+__device__ __forceinline__ void spin_watchdog(unsigned &n, unsigned long long &t0) {
+    if ((++n & 4095u) != 0u) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t0 == 0) t0 = t;
+    else if (t - t0 > 10000000000ull) __trap();
+}
+
 __device__ __forceinline__ void wait_flag(const int *f) {
+    unsigned n = 0;
+    unsigned long long t0 = 0;
     while (ld_relaxed(f) == 0) {
         if (KPL_IC0_SPIN_NS > 0) __nanosleep(KPL_IC0_SPIN_NS);
+        spin_watchdog(n, t0);
     }
     (void)ld_acquire(f);
 }
@@ -91,8 +105,11 @@ __device__ __forceinline__ void st_relaxed_f64(double *p, double x) {
 
 __device__ __forceinline__ double wait_value(const double *p) {
     double x = ld_relaxed_f64(p);
+    unsigned n = 0;
+    unsigned long long t0 = 0;
     while ((unsigned long long)__double_as_longlong(x) == kIcEmpty) {
         if (KPL_IC0_SPIN_NS > 0) __nanosleep(KPL_IC0_SPIN_NS);
+        spin_watchdog(n, t0);
         x = ld_relaxed_f64(p);
     }
     return x;

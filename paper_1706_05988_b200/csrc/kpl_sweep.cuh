@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(NT, 2)
 stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
     __shared__ __align__(16) double sp[Body::kStencil ? 2 * SMEM_PLANE : 2];
     __shared__ double sred[NQ * NWARP];
+    pdl_wait();
+    pdl_launch_dependents();
     if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
     stencil_pass<VX, In, Body>(g, L, in, body, ws, cfg, phase, sp, sred);
 }
@@ -251,7 +253,13 @@ __device__ __forceinline__ void grid_sync(WsHead *h) {
             atomicAdd(&h->bar_gen, 1u);
         } else {
             volatile unsigned *g = &h->bar_gen;          // poll through L2 without atomics
-            while (*g == gen) {
+            unsigned long long t0 = 0, t;
+            for (unsigned n = 1; *g == gen; ++n) {
+                if ((n & 4095u) == 0u) {                  // watchdog: a broken barrier traps, not hangs
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    if (t0 == 0) t0 = t;
+                    else if (t - t0 > 10000000000ull) __trap();
+                }
             }
         }
         __threadfence();

@@ -123,6 +123,8 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
     unsigned long long *sempty = wempty + SW;
     __shared__ double sred[NQ * NWARP];
 
+    pdl_wait();
+    pdl_launch_dependents();
     if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
     body.setup(ws);
     const long long par = wsel ? (ws.head->iter & 1) : 0;    // w_in = w[iter & 1] (ping-pong) or fixed
