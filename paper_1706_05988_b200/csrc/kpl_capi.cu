@@ -248,12 +248,12 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
             g_launches.fetch_add(1, std::memory_order_relaxed);
             const unsigned sgrid = (unsigned)std::min(L.items, cap);
             if constexpr (std::is_same<SpIn, NoSpmvIn>::value)
-                csr_spmv_kernel<In><<<sgrid, NT, 0, st>>>(g, in, ws.nbuf, ws, pred, row);
+                launch_pdl(csr_spmv_kernel<In>, sgrid, NT, 0, st, g, in, ws.nbuf, ws, pred, row);
             else
-                csr_spmv_kernel<SpIn><<<sgrid, NT, 0, st>>>(g, spin, ws.nbuf, ws, pred, row);
+                launch_pdl(csr_spmv_kernel<SpIn>, sgrid, NT, 0, st, g, spin, ws.nbuf, ws, pred, row);
         }
-        csr_chunk_sweep<In, Body><<<(unsigned)std::min(L.nch, cap), NT, 0, st>>>(g, L, in, body, ws.nbuf, ws, cfg,
-                                                                               phase, pred, row);
+        launch_pdl(csr_chunk_sweep<In, Body>, (unsigned)std::min(L.nch, cap), NT, 0, st, g, L, in, body,
+                   (const double *)ws.nbuf, ws, cfg, phase, pred, row);
     }
     if (ws.prod && phase != PH_NONE && Body::NQ > 0) {
         g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -457,6 +457,8 @@ __global__ void __launch_bounds__(NT, KPL_SPMV_MINB)
 csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
     constexpr int PER = CSR_WIN / NT;
     __shared__ double sprod[CSR_WIN];
+    pdl_wait();
+    pdl_launch_dependents();
     if (ws.head && !pred_ok(ws.head, pred, row)) return;
     if (ws.head) in.setup(ws);
     const int tid = threadIdx.x;
@@ -507,6 +509,8 @@ csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ n
     constexpr int Q = Body::NQ;
     __shared__ double sred[NQ * NWARP];
     __shared__ double sitem[Q > 0 ? Q : 1][64];
+    pdl_wait();
+    pdl_launch_dependents();
     if (!pred_ok(ws.head, pred, row)) return;
     body.setup(ws);
     in.setup(ws);
