@@ -3,8 +3,9 @@
 
 BASELINE.json metric / config 3: 7-point Laplacian on 512^3 (134,217,728 DOF),
 matrix-free, unpreconditioned, b = A * (1/sqrt(n)), x0 = 0, fixed 500 p-CG-sh
-iterations (rtol 0), sigma = 2.30188679245283 (the value the reference's
-selection rule gives at 32^3..128^3).
+iterations (rtol 0), sigma = 2.30188679245283 (the reference's selection rule
+on the 500-iteration p-CG history, recomputed at 512^3 on the device:
+tools/sigma_config3.py, profiles/r01_sigma_config3.jsonl).
 
 A "step" is one full solve through the drop-in API (init + 500 fused
 iterations + the reference's true-residual cadence).  `value` is iterations/s
