@@ -64,3 +64,22 @@ def test_choose_shift_on_device_history():
     ref = K.solve(A, None, b, None, K.SolverConfig(method="cg", max_iters=2000, rtol=1e-12))
     assert res.converged and abs(res.iterations - ref.iterations) <= 0.02 * ref.iterations
     assert res.history[-1].rnorm_true <= 2.0 * ref.history[-1].rnorm_true
+
+
+@pytest.mark.gpu
+def test_config3_rule_at_32cubed_reference_order():
+    """Config 3's selection workflow (500 p-CG iterations, default grid, margin
+    rule) on the device in the reference reduction order at 32^3 gives the
+    sigma of SURVEY.md B.6 (2.30188679245283; argmin psi 9.245) -- the value
+    bench.py uses at 512^3, where tools/sigma_config3.py recomputes it."""
+    import math
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    A = K.Stencil3D(32, 32, 32)
+    b = K.spmv(A, np.full(A.n, 1.0 / math.sqrt(A.n)))
+    with K.reduction_order("reference"):
+        sigma, sw, base = S.choose_shift(A, None, b, max_iters=500, rtol=0.0)
+    assert base.iterations == 500
+    assert sigma == 2.30188679245283
+    assert abs(sw.argmin - 9.245) < 5e-4
