@@ -717,3 +717,39 @@ def test_peer_exchange_schedule_is_fresh_and_race_free(monkeypatch, method, extr
         elif e[0] == "fin":
             since_fin = True
     assert since_fin
+
+
+@gpu
+@pytest.mark.parametrize("kind", ["slab", "rows"])
+def test_local_peer_eight_ranks_bitwise(kind):
+    """Eight virtual ranks (the 8 x B200 box layout) through the peer exchange:
+    bit-identical to one GPU for a z-slab stencil and a CSR row-block matrix."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200 import problems
+    from paper_1706_05988_b200.distributed import LocalPeerComm, solve_distributed
+    P = 8
+    if kind == "slab":
+        A = K.Stencil3D(64, 24, 32)
+        b = K.spmv(A, np.random.default_rng(2).normal(size=A.n))
+        cfg = K.SolverConfig(method="pcg_sh", shift=2.30188679245283, max_iters=80, rtol=1e-10)
+        ref = _one_gpu(A, None, b, cfg, 4)
+        plan = SlabPlan(64, 24, 32, P, 4)
+        res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
+                                comm=LocalPeerComm(P), zc=4)
+        M = None
+    else:
+        A = problems.banded_spd(20000, seed=0, band=2000)
+        M = K.make_jacobi(A)
+        b = K.spmv(A, np.random.default_rng(1).standard_normal(A.n))
+        cfg = K.SolverConfig(method="pcg_sh", shift=0.4124626382901352, max_iters=300, rtol=1e-10)
+        ref = K.solve(A, M, b, None, cfg)
+        plan = RowPlan(A, P)
+        res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
+                                comm=LocalPeerComm(P))
+    x = np.concatenate([xi.cpu().numpy() for xi in res.x])
+    assert res.iterations == ref.iterations
+    assert [(h.alpha, h.beta, h.rnorm_true) for h in res.history] == \
+           [(h.alpha, h.beta, h.rnorm_true) for h in ref.history]
+    assert x.tobytes() == np.asarray(ref.x).tobytes()
