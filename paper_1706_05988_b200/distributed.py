@@ -875,6 +875,11 @@ class DistributedSolve:
             raise _lib.KplError(f"distributed solve ended in state {st.state}")
         rows = int(st.iter) + 1
         if np.isnan(s0.history(rows)[-1, 5]):
+            if self.peer:
+                # sweeps issued past convergence were predicated off on the device,
+                # so the halos a fused sweep would have pushed were never sent:
+                # re-push whatever the final record reads
+                self._dirty.update(self._names)
             self.record(int(st.iter), cadence_only=False)
             if self.peer:
                 self._flush()

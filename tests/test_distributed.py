@@ -753,3 +753,24 @@ def test_local_peer_eight_ranks_bitwise(kind):
     assert [(h.alpha, h.beta, h.rnorm_true) for h in res.history] == \
            [(h.alpha, h.beta, h.rnorm_true) for h in ref.history]
     assert x.tobytes() == np.asarray(ref.x).tobytes()
+
+
+@gpu
+def test_fused_final_record_after_predicated_sweeps():
+    """Regression (found by tools/fuzz_parity.py dist): sweeps enqueued past
+    convergence are predicated off on the device, so the x halo a fused sweep
+    would push for the next cadence row never arrives; the final true-residual
+    record must re-push it.  Converges at row 67, not a cadence row."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200.distributed import LocalPeerComm, solve_distributed
+    A = K.Stencil3D(16, 9, 9)
+    b = np.random.default_rng(0).standard_normal(A.n)
+    cfg = K.SolverConfig(method="pcg_sh", shift=0.75, max_iters=110, rtol=1e-12)
+    ref = _one_gpu(A, None, b, cfg, 1)
+    plan = SlabPlan(16, 9, 9, 3, 1)
+    res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(3)], None, cfg,
+                            comm=LocalPeerComm(3), zc=1)
+    assert res.iterations == ref.iterations and ref.iterations % 10 != 0
+    assert [(h.alpha, h.rnorm_true) for h in res.history] == [(h.alpha, h.rnorm_true) for h in ref.history]

@@ -2,7 +2,7 @@
 layout), bitwise: random stencil shapes / CSR matrices, methods, shifts,
 preconditioners, x0, gaps; breakdowns must match too.
 
-    python tools/fuzz_parity.py [cases] [seed]
+    python tools/fuzz_parity.py [cases] [seed] [tree|reference|dist]
 """
 import os
 import sys
@@ -72,24 +72,102 @@ def check_case(A, jac, kw, b, x0):
     return ok
 
 
-def run(cases, seed, log=print):
-    """Descriptions of the failing cases."""
+def check_case_reference_order(A, jac, kw, b, x0):
+    """Reference reduction order (single GPU) vs the oracle with the
+    reference's own blocked_dot: bit for bit."""
+    M = K.make_jacobi(A) if jac else None
+    Mo = O.make_jacobi(O.as_oracle_operator(A)) if jac else None
+    res = err = ores = oerr = None
+    try:
+        with K.reduction_order("reference"):
+            res = K.solve(A, M, b, x0, K.SolverConfig(**kw))
+    except Exception as e:
+        err = e
+    try:
+        ores = O.solve(O.as_oracle_operator(A), Mo, b, x0, O.Config(**kw))
+    except Exception as e:
+        oerr = e
+    if err is not None or oerr is not None:
+        return type(err).__name__ == type(oerr).__name__ and str(err) == str(oerr)
+    return (res.iterations == ores.iterations and same_bits(hist6(res), oracle_hist6(ores))
+            and same_bits(np.asarray(res.x), ores.x) and res.replacements == list(ores.replacements))
+
+
+INFO = [""]
+
+
+def check_case_distributed(A, jac, kw, b, x0, rng):
+    """P virtual ranks through the fused peer exchange vs one GPU, bit for bit
+    (x0 is not part of the partitioned entry point's test here)."""
+    from paper_1706_05988_b200.distributed import LocalPeerComm, RowPlan, SlabPlan, solve_distributed
+    from paper_1706_05988_b200.solvers import _Solve
+    M = K.make_jacobi(A) if jac else None
+    cfg = K.SolverConfig(**kw)
+    if hasattr(A, "stencil_spec"):
+        NX, NY, NZ, _ = A.slab_spec() if hasattr(A, "slab_spec") else A.stencil_spec()
+        Ps = [p for p in (2, 3, 4, 8) if NZ % p == 0]
+        if not Ps:
+            return None                      # not partitionable: skipped
+        P = int(rng.choice(Ps))
+        nzl = NZ // P
+        zc = max(z for z in (1, 2, 4, 8) if nzl % z == 0)
+        plan = SlabPlan(NX, NY, NZ, P, zc)
+        comm = LocalPeerComm(P, fused=bool(rng.integers(2)))
+        INFO[0] = f"dims={(NX, NY, NZ)} P={P} zc={zc} fused={comm.fused} kw={kw}"
+        try:
+            ref = _Solve(A, M, b, None, cfg, zc=zc, slab_view=True).run()
+            res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg, comm=comm, zc=zc)
+        except Exception as e:
+            return "Breakdown" in type(e).__name__
+    else:
+        if A.n < 2 * 256:
+            return None
+        P = int(rng.integers(2, min(8, A.n // 256) + 1))
+        try:
+            plan = RowPlan(A, P, chunk_blocks=1)
+        except ValueError:
+            return None
+        comm = LocalPeerComm(P, fused=bool(rng.integers(2)))
+        try:
+            ref = _Solve(A, M, b, None, cfg, chunk_blocks=1).run()
+            res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg, comm=comm,
+                                    chunk_blocks=1)
+        except Exception as e:
+            return "Breakdown" in type(e).__name__
+    x = np.concatenate([xi.cpu().numpy() for xi in res.x])
+    return (res.iterations == ref.iterations and same_bits(hist6(res), hist6(ref))
+            and same_bits(x, np.asarray(ref.x)) and res.replacements == ref.replacements)
+
+
+def run(cases, seed, log=print, mode="tree"):
+    """Descriptions of the failing cases (mode: tree | reference | dist)."""
     rng = np.random.default_rng(seed)
     failures = []
+    skipped = 0
     for c in range(cases):
         A, jac, kw, b, x0, desc = random_case(rng)
         try:
-            ok = check_case(A, jac, kw, b, x0)
+            if mode == "reference":
+                ok = check_case_reference_order(A, jac, kw, b, x0)
+            elif mode == "dist":
+                ok = check_case_distributed(A, jac, kw, b, x0, rng)
+            else:
+                ok = check_case(A, jac, kw, b, x0)
         except Exception:
             ok = False
             log(traceback.format_exc())
-        if not ok:
-            failures.append(f"case {c}: {desc}")
+        if ok is None:
+            skipped += 1
+        elif not ok:
+            failures.append(f"case {c}: {desc} {INFO[0] if mode == 'dist' else ''}")
             log("MISMATCH", failures[-1])
+    if skipped:
+        log(f"({skipped} of {cases} cases not applicable in mode {mode})")
     return failures
 
 
 if __name__ == "__main__":
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-    fails = run(cases, int(sys.argv[2]) if len(sys.argv) > 2 else 0)
-    print(f"fuzz parity: {len(fails)}/{cases} failing", flush=True)
+    mode = sys.argv[3] if len(sys.argv) > 3 else "tree"
+    fails = run(cases, int(sys.argv[2]) if len(sys.argv) > 2 else 0, mode=mode)
+    print(f"fuzz parity ({mode}): {len(fails)}/{cases} failing", flush=True)
