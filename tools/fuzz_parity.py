@@ -97,12 +97,16 @@ INFO = [""]
 
 
 def check_case_distributed(A, jac, kw, b, x0, rng):
-    """P virtual ranks through the fused peer exchange vs one GPU, bit for bit
-    (x0 is not part of the partitioned entry point's test here)."""
-    from paper_1706_05988_b200.distributed import LocalPeerComm, RowPlan, SlabPlan, solve_distributed
+    """P virtual ranks (host NCCL-style exchange, fused or post-kernel peer
+    exchange) vs one GPU, bit for bit."""
+    from paper_1706_05988_b200.distributed import LocalComm, LocalPeerComm, RowPlan, SlabPlan, solve_distributed
     from paper_1706_05988_b200.solvers import _Solve
     M = K.make_jacobi(A) if jac else None
     cfg = K.SolverConfig(**kw)
+    kinds = [lambda P: LocalComm(P), lambda P: LocalPeerComm(P), lambda P: LocalPeerComm(P, fused=False)]
+    make_comm = kinds[int(rng.integers(3))]
+    comm_name = lambda c: type(c).__name__ + ("" if not hasattr(c, "fused") else f"(fused={c.fused})")
+    split = lambda v, plan, P: None if v is None else [v[plan.local_slice(r)] for r in range(P)]
     if hasattr(A, "stencil_spec"):
         NX, NY, NZ, _ = A.slab_spec() if hasattr(A, "slab_spec") else A.stencil_spec()
         Ps = [p for p in (2, 3, 4, 8) if NZ % p == 0]
@@ -112,11 +116,12 @@ def check_case_distributed(A, jac, kw, b, x0, rng):
         nzl = NZ // P
         zc = max(z for z in (1, 2, 4, 8) if nzl % z == 0)
         plan = SlabPlan(NX, NY, NZ, P, zc)
-        comm = LocalPeerComm(P, fused=bool(rng.integers(2)))
-        INFO[0] = f"dims={(NX, NY, NZ)} P={P} zc={zc} fused={comm.fused} kw={kw}"
+        comm = make_comm(P)
+        INFO[0] = f"dims={(NX, NY, NZ)} P={P} zc={zc} comm={comm_name(comm)} kw={kw}"
         try:
-            ref = _Solve(A, M, b, None, cfg, zc=zc, slab_view=True).run()
-            res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg, comm=comm, zc=zc)
+            ref = _Solve(A, M, b, x0, cfg, zc=zc, slab_view=True).run()
+            res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], split(x0, plan, P), cfg,
+                                    comm=comm, zc=zc)
         except Exception as e:
             return "Breakdown" in type(e).__name__
     else:
@@ -127,11 +132,12 @@ def check_case_distributed(A, jac, kw, b, x0, rng):
             plan = RowPlan(A, P, chunk_blocks=1)
         except ValueError:
             return None
-        comm = LocalPeerComm(P, fused=bool(rng.integers(2)))
+        comm = make_comm(P)
+        INFO[0] = f"P={P} comm={comm_name(comm)} kw={kw}"
         try:
-            ref = _Solve(A, M, b, None, cfg, chunk_blocks=1).run()
-            res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg, comm=comm,
-                                    chunk_blocks=1)
+            ref = _Solve(A, M, b, x0, cfg, chunk_blocks=1).run()
+            res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], split(x0, plan, P), cfg,
+                                    comm=comm, chunk_blocks=1)
         except Exception as e:
             return "Breakdown" in type(e).__name__
     x = np.concatenate([xi.cpu().numpy() for xi in res.x])
