@@ -33,7 +33,7 @@ def random_case(rng):
         A = problems.banded_spd(int(rng.integers(300, 30000)), seed=int(rng.integers(1000)),
                                 band=int(rng.integers(2, 400)))
     method = str(rng.choice(["cg", "pcg", "pcg_sh", "pcg_rr", "pcg_var_sh"]))
-    jac = bool(rng.integers(2))
+    jac = str(rng.choice(["none", "jacobi", "ic0"], p=[0.4, 0.4, 0.2]))
     gaps = bool(rng.integers(4) == 0)
     maxit = int(rng.integers(1, 120))
     kw = dict(method=method, max_iters=maxit, rtol=float(rng.choice([0.0, 1e-8, 1e-12])), track_gaps=gaps)
@@ -49,17 +49,30 @@ def random_case(rng):
     return A, jac, kw, b, x0, desc
 
 
+def precs(A, pc):
+    """(device, oracle) preconditioners; IC(0) breakdowns propagate."""
+    if pc == "jacobi":
+        return K.make_jacobi(A), O.make_jacobi(O.as_oracle_operator(A))
+    if pc == "ic0":
+        Ac = A.to_csr() if hasattr(A, "to_csr") else A
+        return K.make_ic0(A), O.make_ic0(O.as_oracle_operator(Ac))
+    return None, None
+
+
 def check_case(A, jac, kw, b, x0):
     """True when the device and the oracle (device dot order) agree bit for bit."""
-    M = K.make_jacobi(A) if jac else None
-    Mo = O.make_jacobi(O.as_oracle_operator(A)) if jac else None
+    try:
+        M, Mo = precs(A, jac)
+    except Exception:
+        return None                            # IC(0) breakdown of this matrix: nothing to solve
     res = err = ores = oerr = None
     try:
         res = K.solve(A, M, b, x0, K.SolverConfig(**kw))
     except Exception as e:
         err = e
     try:
-        ores = O.solve(A, Mo, b, x0, O.Config(**kw), dot=gpu_dot(A))
+        Ao = A.to_csr() if (jac == "ic0" and hasattr(A, "to_csr")) else A   # IC(0) runs the CSR form
+        ores = O.solve(Ao, Mo, b, x0, O.Config(**kw), dot=gpu_dot(Ao))
     except Exception as e:
         oerr = e
     if err is not None or oerr is not None:
@@ -75,8 +88,10 @@ def check_case(A, jac, kw, b, x0):
 def check_case_reference_order(A, jac, kw, b, x0):
     """Reference reduction order (single GPU) vs the oracle with the
     reference's own blocked_dot: bit for bit."""
-    M = K.make_jacobi(A) if jac else None
-    Mo = O.make_jacobi(O.as_oracle_operator(A)) if jac else None
+    try:
+        M, Mo = precs(A, jac)
+    except Exception:
+        return None
     res = err = ores = oerr = None
     try:
         with K.reduction_order("reference"):
@@ -101,7 +116,9 @@ def check_case_distributed(A, jac, kw, b, x0, rng):
     exchange) vs one GPU, bit for bit."""
     from paper_1706_05988_b200.distributed import LocalComm, LocalPeerComm, RowPlan, SlabPlan, solve_distributed
     from paper_1706_05988_b200.solvers import _Solve
-    M = K.make_jacobi(A) if jac else None
+    if jac == "ic0":
+        return None                              # IC(0) is single-GPU
+    M = K.make_jacobi(A) if jac == "jacobi" else None
     cfg = K.SolverConfig(**kw)
     kinds = [lambda P: LocalComm(P), lambda P: LocalPeerComm(P), lambda P: LocalPeerComm(P, fused=False)]
     make_comm = kinds[int(rng.integers(3))]
