@@ -41,7 +41,7 @@ constexpr int SMEM_PLANE = 1548;
 #define KPL_CSR_WIN 1024
 #endif
 #ifndef KPL_SPMV_MINB
-#define KPL_SPMV_MINB 6
+#define KPL_SPMV_MINB 8
 #endif
 constexpr int CSR_WIN = KPL_CSR_WIN;   // staged nonzeros per window
 
@@ -452,11 +452,13 @@ persistent_redundant(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue
 //                    chunk fold (level 3) done in-CTA, one completion atomic per
 //                    chunk.  The item (256 rows) and chunk trees are the ones
 //                    oracle/gpu_order.py emulates.
-template <class In>
+// WIN: staged nonzeros per window (1024 for short rows; 512 for long, randomly
+// gathered rows, where more resident warps beat longer windows); 8 CTAs/SM.
+template <class In, int WIN = CSR_WIN>
 __global__ void __launch_bounds__(NT, KPL_SPMV_MINB)
 csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
-    constexpr int PER = CSR_WIN / NT;
-    __shared__ double sprod[CSR_WIN];
+    constexpr int PER = WIN / NT;
+    __shared__ double sprod[WIN];
     pdl_wait();
     pdl_launch_dependents();
     if (ws.head && !pred_ok(ws.head, pred, row)) return;
@@ -472,8 +474,8 @@ csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long l
     long long lo = 0, hi = 0;
     if (ok) { lo = __ldg(g.row_ptr + r); hi = __ldg(g.row_ptr + r + 1); }
     double a = 0.0;
-    for (long long wk = k0; wk < k1; wk += CSR_WIN) {
-        const long long we = min(wk + (long long)CSR_WIN, k1);
+    for (long long wk = k0; wk < k1; wk += WIN) {
+        const long long we = min(wk + (long long)WIN, k1);
         int col[PER];
         double val[PER], raw[PER];
 #pragma unroll
