@@ -483,10 +483,15 @@ class _Regions:
         self.red = 0            # reductions exchanged (table slot = red & 1)
         self._owned, self._opened = list(owned), list(opened)
 
-    def close(self):
+    def close(self, barrier=None):
+        """Unmap the peers' regions, then (after `barrier`, so no rank still has
+        this rank's region mapped -- freeing an exported allocation while it is
+        open elsewhere is undefined) free this rank's own."""
         lib = _lib.load()
         for p in self._opened:
             lib.kpl_ipc_close(p)
+        if barrier is not None and self._owned:
+            barrier()
         for p in self._owned:
             lib.kpl_ipc_free(p)
         self._owned, self._opened, self.tensors = [], [], {}
@@ -541,7 +546,7 @@ class PeerComm(TorchComm):
         if key in self._cache:
             return self._cache[key]
         for r in self._cache.values():
-            r.close()
+            r.close(barrier=lambda: self.dist.barrier(group=self.group))
         self._cache = {}
         import ctypes
         lib = _lib.load()

@@ -535,7 +535,7 @@ def _ipc_post_worker(rank, world, port, q):
         flags = reg[:8 * world].view(torch.int64).cpu().numpy().tolist()
         q.put((rank, ok_lo, ok_hi, slot.tobytes() == want.tobytes(), flags))
         dist.barrier()
-        S.reg.close()
+        S.reg.close(barrier=dist.barrier)
     except Exception as exc:
         q.put((rank, "error", repr(exc), None, None))
     finally:
