@@ -556,16 +556,25 @@ class PeerComm(TorchComm):
         _lib.check(lib.kpl_ipc_alloc(int(sizes[me]), ctypes.byref(ptr), h), "IPC region")
         handles = [None] * P
         self.dist.all_gather_object(handles, bytes(h.raw), group=self.group)
-        bases, opened = [], []
+        bases, opened, why = [], [], ""
         for q in range(P):
             if q == me:
                 bases.append(ptr.value)
                 continue
             p = ctypes.c_void_p()
-            _lib.check(lib.kpl_ipc_open(ctypes.create_string_buffer(handles[q], 64), ctypes.byref(p)),
-                       f"IPC open of rank {q}")
+            if lib.kpl_ipc_open(ctypes.create_string_buffer(handles[q], 64), ctypes.byref(p)) != 0:
+                why = f"rank {me}: IPC open of rank {q}: {lib.kpl_last_error().decode()}"
+                break
             bases.append(p.value)
             opened.append(p.value)
+        # one collective verdict, so every rank takes the same path
+        verdicts = [None] * P
+        self.dist.all_gather_object(verdicts, why, group=self.group)
+        bad = [v for v in verdicts if v]
+        if bad:
+            _Regions({}, [], owned=[ptr.value], opened=opened).close(
+                barrier=lambda: self.dist.barrier(group=self.group))
+            raise _lib.KplError("peer exchange unavailable: " + "; ".join(bad))
         t = D.torch()
         tens = {me: t.as_tensor(_CudaArray(ptr.value, int(sizes[me])), device=device)}
         self._cache[key] = _Regions(tens, bases, owned=[ptr.value], opened=opened)
