@@ -308,13 +308,18 @@ def run_distributed(args, rank, world, local):
     exchange = os.environ.get("KPL_DIST_EXCHANGE", "peer" if dist.get_backend() == "nccl" else "host")
     comm = None
     if exchange == "peer":
+        why = ""
         try:
             comm = PeerComm()
             solve_distributed(A, None, b, None, K.SolverConfig(method="pcg_sh", shift=SIGMA, max_iters=2,
                                                                rtol=0.0), comm=comm)
-        except Exception as exc:          # IPC unavailable: report and use the host-driven path
-            print(f"[bench] peer exchange unavailable ({exc}); using NCCL send/recv + all-gather",
-                  file=sys.stderr)
+        except Exception as exc:          # IPC unavailable: use the host-driven path (all ranks)
+            why = f"rank {rank}: {exc}"
+        verdicts = [None] * world
+        dist.all_gather_object(verdicts, why)
+        if any(verdicts):
+            print(f"[bench] peer exchange unavailable ({'; '.join(v for v in verdicts if v)}); "
+                  "using NCCL send/recv + all-gather", file=sys.stderr)
             comm, exchange = None, "host"
     if comm is None:
         comm = TorchComm()
