@@ -12,6 +12,7 @@
 // `cen` is the raw stencil input at k (the register queue's centre), so the
 // update never re-reads it from memory.
 #pragma once
+#include <type_traits>
 #include "kpl_core.cuh"
 
 namespace kpl {
@@ -69,6 +70,22 @@ struct InVec {
         else return r;
     }
 };
+
+// One-element load of a CSR operand (gather or row centre).  L2G: plain
+// vectors are read L2-direct (ld.global.cg) with no runtime branch on
+// `coherent`; other inputs (e.g. classic CG's p = axpy(beta, p, u)) use raw().
+template <class T> struct is_invec : std::false_type {};
+template <int PC> struct is_invec<InVec<PC>> : std::true_type {};
+template <bool L2G, class In>
+__device__ __forceinline__ double load1(const In &in, const double *p, long long k) {
+    if constexpr (L2G && is_invec<In>::value) {
+        return __ldcg(p + k);
+    } else {
+        double t[1];
+        in.template raw<1>(p, k, t);
+        return t[0];
+    }
+}
 
 // Classic CG direction evaluated where the stencil needs it:
 // p_new = axpy(beta, p_old, u) = beta*p_old + u (beta == 0 -> u), solvers.py:269.

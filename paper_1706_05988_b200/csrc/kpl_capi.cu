@@ -249,17 +249,21 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
             const unsigned sgrid = (unsigned)std::min(L.items, cap);
             // long rows with scattered columns (> 16 nonzeros per row on average): shorter
             // windows, more resident warps for the gathers (config 5: 0.303 -> 0.296 ms)
+            // short rows (structured matrices): gathers L2-direct (configs 2-CSR, 4: -4 %); long
+            // scattered rows keep the read-only path (ld.global.nc is 3 % faster on config 5)
             const bool long_rows = op->nnz > 16 * op->n;
             if constexpr (std::is_same<SpIn, NoSpmvIn>::value) {
                 if (long_rows) launch_pdl(csr_spmv_kernel<In, 512>, sgrid, NT, 0, st, g, in, ws.nbuf, ws, pred, row);
-                else launch_pdl(csr_spmv_kernel<In>, sgrid, NT, 0, st, g, in, ws.nbuf, ws, pred, row);
+                else launch_pdl(csr_spmv_kernel<In, CSR_WIN, true>, sgrid, NT, 0, st, g, in, ws.nbuf, ws, pred, row);
             } else {
                 if (long_rows)
                     launch_pdl(csr_spmv_kernel<SpIn, 512>, sgrid, NT, 0, st, g, spin, ws.nbuf, ws, pred, row);
-                else launch_pdl(csr_spmv_kernel<SpIn>, sgrid, NT, 0, st, g, spin, ws.nbuf, ws, pred, row);
+                else
+                    launch_pdl(csr_spmv_kernel<SpIn, CSR_WIN, true>, sgrid, NT, 0, st, g, spin, ws.nbuf, ws, pred,
+                               row);
             }
         }
-        launch_pdl(csr_chunk_sweep<In, Body>, (unsigned)std::min(L.nch, cap), NT, 0, st, g, L, in, body,
+        launch_pdl(csr_chunk_sweep<In, Body, true>, (unsigned)std::min(L.nch, cap), NT, 0, st, g, L, in, body,
                    (const double *)ws.nbuf, ws, cfg, phase, pred, row);
     }
     if (ws.prod && phase != PH_NONE && Body::NQ > 0) {

@@ -454,7 +454,7 @@ persistent_redundant(SGeo g, Layout L, InW in_w, BodyIt body, InX in_x, BodyTrue
 //                    oracle/gpu_order.py emulates.
 // WIN: staged nonzeros per window (1024 for short rows; 512 for long, randomly
 // gathered rows, where more resident warps beat longer windows); 8 CTAs/SM.
-template <class In, int WIN = CSR_WIN>
+template <class In, int WIN = CSR_WIN, bool L2G = false>
 __global__ void __launch_bounds__(NT, KPL_SPMV_MINB)
 csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
     constexpr int PER = WIN / NT;
@@ -488,7 +488,7 @@ csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long l
         for (int j = 0; j < PER; ++j) {
             const long long kk = wk + tid + (long long)j * NT;
             raw[j] = 0.0;
-            if (kk < we) { double t[1]; in.template raw<1>(in.base(), col[j], t); raw[j] = t[0]; }
+            if (kk < we) raw[j] = load1<L2G>(in, in.base(), col[j]);
         }
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -504,7 +504,7 @@ csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long l
     }
 }
 
-template <class In, class Body>
+template <class In, class Body, bool L2G = false>
 __global__ void __launch_bounds__(NT, 3)
 csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ nin, Ws ws, Cfg cfg, int phase,
                 int pred, long long row) {
@@ -530,9 +530,7 @@ csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ n
             body.template load<1>(r, RR);
             if constexpr (Body::kStencil) {
                 n1 = __ldcs(nin + r);
-                double t[1];
-                in.template raw<1>(in.base(), r, t);
-                c1 = t[0];
+                c1 = load1<L2G>(in, in.base(), r);
             }
         }
     };
