@@ -42,27 +42,30 @@ struct InNone {
 // Raw vector (optionally a ping-pong pair); PC selects the transform:
 //   KPL_PC_IDENTITY: m = w;  KPL_PC_JACOBI_CONST: m = w*c;  KPL_PC_JACOBI_VEC: m = w*d[k]
 // (precond.py:88-89 computes v * inv_diag elementwise: one rounding).
-template <int PC>
+// COH (compile time): 0 = read-only path (ld.global.nc); 1 = through L2 only
+// (ld.global.cg) -- for vectors written earlier in the same kernel (persistent
+// solvers).  A compile-time choice: a runtime flag tested per load kept the
+// compiler from batching the loads (the CSR gathers ran 7 % slower with it).
+template <int PC, int COH = 0>
 struct InVec {
     const double *a0, *a1;
     int sel;
     double c;
     const double *dinv;
     const double *a;
-    int coherent;          // 1: read through L2 (the vector was written earlier in this kernel)
     __device__ void setup(const Ws &ws) { a = pick(ws.head, sel, a0, a1); }
     __device__ const double *base() const { return a; }
     template <int V> __device__ void raw(const double *p, long long k, double (&o)[V]) const {
-        if (coherent) {
+        if constexpr (COH == 1) {
             if constexpr (V == 2) {
                 const double2 t = __ldcg(reinterpret_cast<const double2 *>(p + k));
                 o[0] = t.x; o[1] = t.y;
             } else {
                 o[0] = __ldcg(p + k);
             }
-            return;
+        } else {
+            ld_ro<V>(p, k, o);
         }
-        ld_ro<V>(p, k, o);
     }
     __device__ double xf(double r, long long k) const {
         if constexpr (PC == KPL_PC_JACOBI_CONST) return __dmul_rn(r, c);
@@ -73,9 +76,9 @@ struct InVec {
 
 // One-element load of a CSR operand (gather or row centre).  L2G: plain
 // vectors are read L2-direct (ld.global.cg) with no runtime branch on
-// `coherent`; other inputs (e.g. classic CG's p = axpy(beta, p, u)) use raw().
+// the cache policy; other inputs (e.g. classic CG's p = axpy(beta, p, u)) use raw().
 template <class T> struct is_invec : std::false_type {};
-template <int PC> struct is_invec<InVec<PC>> : std::true_type {};
+template <int PC, int COH> struct is_invec<InVec<PC, COH>> : std::true_type {};
 template <bool L2G, class In>
 __device__ __forceinline__ double load1(const In &in, const double *p, long long k) {
     if constexpr (L2G && is_invec<In>::value) {

@@ -273,11 +273,10 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
     return cuda_check("sweep launch");
 }
 
-template <int PC>
-InVec<PC> in_vec(const kpl_op *op, const double *a0, const double *a1, int sel) {
-    InVec<PC> in;
+template <int PC, int COH = 0>
+InVec<PC, COH> in_vec(const kpl_op *op, const double *a0, const double *a1, int sel) {
+    InVec<PC, COH> in;
     in.a0 = a0; in.a1 = a1; in.sel = sel; in.c = op->pc_const; in.dinv = op->inv_diag; in.a = a0;
-    in.coherent = 0;
     return in;
 }
 
@@ -960,14 +959,12 @@ int kpl_solver_iterate_persistent(const kpl_op *op, const kpl_cfg *cfgp, const k
     SGeo g{op->nx, op->ny, op->nz, op->diag, op->halo_lo, op->halo_hi, op->zhalo};
     BodyTrue tb;
     tb.b = v->b;
-    auto in_x = in_vec<KPL_PC_IDENTITY>(op, v->x, v->x, SEL_FIXED);
-    in_x.coherent = 1;
+    auto in_x = in_vec<KPL_PC_IDENTITY, 1>(op, v->x, v->x, SEL_FIXED);   // L2-direct: written in-kernel
     return with_pc(op, [&](auto pc) -> int {
         constexpr int PC = decltype(pc)::value;
         auto go = [&](auto body) -> int {
             using B = decltype(body);
-            auto in_w = in_vec<PC>(op, v->w0, v->w1, SEL_ITER);
-            in_w.coherent = 1;
+            auto in_w = in_vec<PC, 1>(op, v->w0, v->w1, SEL_ITER);
             body.x = v->x; body.r = v->r; body.u = v->u; body.z = v->z; body.q = v->q;
             body.s = v->s; body.t = v->t; body.p = v->p; body.w0 = v->w0; body.w1 = v->w1;
             body.dinv = op->inv_diag; body.c = op->pc_const; body.sigma = c.sigma; body.dsig = 0.0;

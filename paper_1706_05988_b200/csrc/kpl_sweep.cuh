@@ -240,7 +240,7 @@ stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int
 // boundary after every pass (the last CTA's scalar epilogue must be visible
 // before anybody reads alpha/beta).  Same passes, items and trees as the
 // per-iteration launches, so results are bit-identical.  Stencil-input loads
-// go through L2 (InVec::coherent) because neighbours' values were written
+// go through L2 (InVec<PC, 1>) because neighbours' values were written
 // earlier in the same kernel.
 __device__ __forceinline__ void grid_sync(WsHead *h) {
     __syncthreads();
