@@ -98,6 +98,20 @@ typedef struct kpl_op {
        order (from kpl_ic0_levels, rows sorted by level); NULL = natural     */
     const int32_t *ic_l_order;
     const int32_t *ic_u_order;
+    /* CSR, optional column-sorted gather layout of the SpMV (NULL = gather in
+       CSR order).  Rows are grouped in blocks of sp_rows; block b's nonzeros
+       (row_ptr[b*sp_rows] .. row_ptr[min((b+1)*sp_rows, n)]) are stored sorted
+       by column: sp_col[k] and sp_val[k] are col_idx/values of the entry whose
+       position inside the block, in CSR order, is sp_dest[k].  The SpMV gathers
+       its input in column order (a warp's lanes share cache lines) into shared
+       memory at sp_dest and sums every row left to right from there, so the
+       result is bit-identical to csr_matvec (_kernels.py:44-52).  sp_max = the
+       largest block's nonzero count (<= 65535; shared memory 8*sp_max bytes). */
+    const int32_t  *sp_col;
+    const double   *sp_val;
+    const uint16_t *sp_dest;
+    int32_t sp_rows;
+    int32_t sp_max;
 } kpl_op;
 
 #define KPL_ORDER_TREE      0
@@ -309,6 +323,11 @@ typedef struct kpl_post {
                                                    rank's flag array (incl. own)  */
     unsigned int *counter;                      /* local device word, initially 0,
                                                    self-resetting                 */
+    const void *status;                         /* this rank's workspace (its head):
+                                                   once its exchange has failed the
+                                                   post signals epoch | 2^63 (poison)
+                                                   so every peer fails fast; NULL =
+                                                   never poison                   */
 } kpl_post;
 
 /* Fused form for the hot sweep (stencil z-slabs, KPL_SW_ITER): the sweep
@@ -322,7 +341,7 @@ typedef struct kpl_post {
 #define KPL_PUSH_X 2     /* x (next record's true-residual cadence input)      */
 
 typedef struct kpl_peer_sweep {
-    int32_t   nranks, _pad;
+    int32_t   nranks, rank;
     double   *table[2][KPL_PEER_MAX_RANKS];     /* every rank's table slot, by parity */
     uint64_t *signal[KPL_PEER_MAX_RANKS];       /* as kpl_post.signal                 */
     const double *w_src[2];                     /* local interiors of w0, w1          */
@@ -330,17 +349,30 @@ typedef struct kpl_peer_sweep {
                                                    global boundary)                  */
     const double *x_src;
     double   *x_lo, *x_hi;
+    const uint64_t *flags;                      /* THIS rank's flag array (one word per
+                                                   rank; for the deferred fold)     */
 } kpl_peer_sweep;
 
+/* wait_epoch != 0: deferred fold.  The previous sweep was a fused iteration
+   sweep of the same solve whose exchange (epoch wait_epoch, table slot
+   wait_parity) has NOT been finalised: instead of a kpl_peer_finalize launch
+   in between, every CTA of this sweep waits for the flags, folds the slot and
+   runs the scalar epilogue itself (the paper's reduction overlap,
+   PAPER.md:43-45); results are bit-identical to sweep + finalize.          */
 int kpl_sweep_peer(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, int32_t kind, int64_t row,
                    void *workspace, const kpl_peer_sweep *px, uint64_t epoch, int32_t table_parity,
-                   int32_t push, int32_t wpar, void *stream);
+                   int32_t push, int32_t wpar, uint64_t wait_epoch, int32_t wait_parity, void *stream);
+/* Limit of every device-side peer wait (default 20 s; KPL_PEER_TIMEOUT_S is
+   read at load time).  A wait that times out turns the device status into
+   BREAKDOWN "peer exchange timeout"; a rank that sees a peer's poison,
+   "peer rank failed".                                                       */
+int kpl_set_peer_timeout(double seconds);
 /* Enqueue the copies of `post`, then (after a system-scope fence) store
    `epoch` into every signal word.  Host-side `post` is passed by value.    */
 int kpl_peer_post(const kpl_post *post, uint64_t epoch, void *stream);
-/* Wait until flags[0..nranks) >= epoch (acquire, system scope; a 20 s
+/* Wait until flags[0..nranks) >= epoch (acquire, system scope; the peer
    timeout turns the device status into BREAKDOWN with bd_code 7, "peer
-   exchange timeout"), then, for a reducing sweep `kind` (0 = wait only),
+   exchange timeout", a peer's poison into bd_code 9, "peer rank failed"), then, for a reducing sweep `kind` (0 = wait only),
    fold `table` (chunks_global x 4 doubles) and run the sweep's scalar
    epilogue, as kpl_finalize_global does.                                  */
 int kpl_peer_finalize(const kpl_op *op, const kpl_cfg *cfg, int32_t kind, int64_t row, void *workspace,

@@ -42,7 +42,8 @@ class KplOp(ctypes.Structure):
                 ("chunk_offset", _i64), ("chunks_global", _i64), ("order", _i32), ("_reserved", _i32),
                 ("ic_l_row_ptr", _p), ("ic_l_col_idx", _p), ("ic_l_values", _p),
                 ("ic_u_row_ptr", _p), ("ic_u_col_idx", _p), ("ic_u_values", _p),
-                ("ic_l_order", _p), ("ic_u_order", _p)]
+                ("ic_l_order", _p), ("ic_u_order", _p),
+                ("sp_col", _p), ("sp_val", _p), ("sp_dest", _p), ("sp_rows", _i32), ("sp_max", _i32)]
 
 
 class KplCfg(ctypes.Structure):
@@ -69,16 +70,16 @@ class KplCopy(ctypes.Structure):
 
 class KplPost(ctypes.Structure):
     _fields_ = [("ncopies", _i32), ("nsignals", _i32), ("copies", KplCopy * KPL_PEER_MAX_COPIES),
-                ("signal", _p * KPL_PEER_MAX_RANKS), ("counter", _p)]
+                ("signal", _p * KPL_PEER_MAX_RANKS), ("counter", _p), ("status", _p)]
 
 
 KPL_PUSH_W, KPL_PUSH_X = 1, 2
 
 
 class KplPeerSweep(ctypes.Structure):
-    _fields_ = [("nranks", _i32), ("_pad", _i32), ("table", (_p * KPL_PEER_MAX_RANKS) * 2),
+    _fields_ = [("nranks", _i32), ("rank", _i32), ("table", (_p * KPL_PEER_MAX_RANKS) * 2),
                 ("signal", _p * KPL_PEER_MAX_RANKS), ("w_src", _p * 2), ("w_lo", _p * 2), ("w_hi", _p * 2),
-                ("x_src", _p), ("x_lo", _p), ("x_hi", _p)]
+                ("x_src", _p), ("x_lo", _p), ("x_hi", _p), ("flags", _p)]
 
 
 _SIGS = {
@@ -119,7 +120,8 @@ _SIGS = {
     "kpl_peer_finalize": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), _i32, _i64, _p, _p, _p, _i32,
                                  ctypes.c_uint64, _p]),
     "kpl_sweep_peer": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg), ctypes.POINTER(KplVecs), _i32,
-                              _i64, _p, _p, ctypes.c_uint64, _i32, _i32, _i32, _p]),
+                              _i64, _p, _p, ctypes.c_uint64, _i32, _i32, _i32, ctypes.c_uint64, _i32, _p]),
+    "kpl_set_peer_timeout": (_i32, [_d]),
     "kpl_ipc_alloc": (_i32, [_i64, ctypes.POINTER(_p), _p]),
     "kpl_ipc_open": (_i32, [_p, ctypes.POINTER(_p)]),
     "kpl_ipc_close": (_i32, [_p]),

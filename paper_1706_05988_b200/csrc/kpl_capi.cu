@@ -28,6 +28,12 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<long long> g_launches{0};   // kernels this library has launched (bench evidence)
+// limit of every device-side peer wait (kpl_set_peer_timeout; KPL_PEER_TIMEOUT_S at load)
+std::atomic<unsigned long long> g_peer_timeout_ns{[] {
+    const char *e = std::getenv("KPL_PEER_TIMEOUT_S");
+    const double s = e ? std::atof(e) : 20.0;
+    return (unsigned long long)((s > 0.0 ? s : 20.0) * 1e9);
+}()};
 
 int fail(int code, const std::string &msg) {
     g_err = msg;
@@ -83,6 +89,9 @@ int make_layout(const kpl_op *op, Layout &L) {
         const long long blocks = cdiv(op->n, RB);
         const int cb = op->chunk_blocks > 0 ? op->chunk_blocks : 8;
         if (cb > 64) return fail(KPL_EINVAL, "chunk_blocks must be <= 64");
+        if (op->sp_col && (!op->sp_val || !op->sp_dest || op->sp_rows < 1 || op->sp_max < 1 ||
+                           op->sp_max > 65535 || 8LL * op->sp_max > 227 * 1024))
+            return fail(KPL_EINVAL, "bad column-sorted SpMV layout");
         L.vx = 1; L.wx = NWARP; L.wy = 1; L.zc = cb;
         L.T = cb;
         L.items = blocks;
@@ -150,6 +159,10 @@ Ws make_ws(const kpl_op *op, const Layout &L, long long max_iters, void *workspa
     ws.px = nullptr;
     ws.epoch = 0;
     ws.tpar = ws.push = ws.wpar = 0;
+    ws.wait_epoch = 0;
+    ws.wait_tpar = 0;
+    ws.timeout_ns = g_peer_timeout_ns.load(std::memory_order_relaxed);
+    ws.final_cnt = &ws.head->final_cnt;
     return ws;
 }
 
@@ -224,6 +237,38 @@ void launch_pdl(Kern kern, unsigned grid, unsigned block, size_t smem, cudaStrea
     cudaLaunchKernelEx(&lc, kern, args...);
 }
 
+// Column-sorted SpMV launch (kpl_op.sp_*): dynamic shared memory of the
+// largest block's products; KPL_SORTED_NT picks the CTA size (tuning knob).
+template <class SIn, int NTS, int PER>
+void launch_sorted_nt(const CGeo &g, const SGather &sg, const SIn &in, double *out, const Ws &ws, int pred,
+                      long long row, unsigned grid, size_t smem, cudaStream_t st) {
+    auto kern = csr_sorted_spmv<SIn, NTS, PER>;
+    if (smem > 48 * 1024)    // per device and cheap: set before every launch
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(kern, grid, NTS, smem, st, g, sg, in, out, ws, pred, row);
+}
+template <class SIn>
+void launch_sorted(const kpl_op *op, const CGeo &g, const SIn &in, double *out, const Ws &ws, int pred,
+                   long long row, cudaStream_t st) {
+    static const int nts = [] { const char *e = std::getenv("KPL_SORTED_NT"); return e ? std::atoi(e) : 512; }();
+    static const int per = [] { const char *e = std::getenv("KPL_SORTED_PER"); return e ? std::atoi(e) : 4; }();
+    const SGather sg{op->sp_col, op->sp_val, reinterpret_cast<const unsigned short *>(op->sp_dest), op->sp_rows};
+    const long long nblk = cdiv(op->n, op->sp_rows);
+    // idle replacement sweeps (PRED_FIRE) keep a small grid, as the other sweeps
+    const size_t smem = 8 * (size_t)op->sp_max;
+    // persistent: one CTA per SM (two when the products fit twice), striding over the
+    // blocks so the next block's first stream loads overlap this block's row sums
+    const long long per_sm = smem > 110 * 1024 ? 1 : 2;
+    const unsigned grid = (unsigned)std::min(nblk, pred == PRED_FIRE ? 2LL * kSMs : per_sm * kSMs);
+    if (nts == 1024) {
+        if (per == 8) launch_sorted_nt<SIn, 1024, 8>(g, sg, in, out, ws, pred, row, grid, smem, st);
+        else launch_sorted_nt<SIn, 1024, 4>(g, sg, in, out, ws, pred, row, grid, smem, st);
+    } else {
+        if (per == 8) launch_sorted_nt<SIn, 512, 8>(g, sg, in, out, ws, pred, row, grid, smem, st);
+        else launch_sorted_nt<SIn, 512, 4>(g, sg, in, out, ws, pred, row, grid, smem, st);
+    }
+}
+
 // `spin`: input of the CSR SpMV when it differs from the body's stencil input
 // (m = w * inv_diag materialised in the workspace); NoSpmvIn = use `in`.
 template <class In, class Body, class SpIn = NoSpmvIn>
@@ -252,7 +297,11 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
             // short rows (structured matrices): gathers L2-direct (configs 2-CSR, 4: -4 %); long
             // scattered rows keep the read-only path (ld.global.nc is 3 % faster on config 5)
             const bool long_rows = op->nnz > 16 * op->n;
-            if constexpr (std::is_same<SpIn, NoSpmvIn>::value) {
+            if (op->sp_col) {
+                // column-sorted gathers (scattered matrices): one CTA per block of sp_rows rows
+                if constexpr (std::is_same<SpIn, NoSpmvIn>::value) launch_sorted(op, g, in, ws.nbuf, ws, pred, row, st);
+                else launch_sorted(op, g, spin, ws.nbuf, ws, pred, row, st);
+            } else if constexpr (std::is_same<SpIn, NoSpmvIn>::value) {
                 if (long_rows) launch_pdl(csr_spmv_kernel<In, 512>, sgrid, NT, 0, st, g, in, ws.nbuf, ws, pred, row);
                 else launch_pdl(csr_spmv_kernel<In, CSR_WIN, true>, sgrid, NT, 0, st, g, in, ws.nbuf, ws, pred, row);
             } else {
@@ -421,6 +470,8 @@ __global__ void head_init_kernel(WsHead *h, double *hist, long long nrows, unsig
         h->bar_cnt = 0u;
         h->bar_gen = 0u;
         h->bar_arrive = 0ull;
+        h->fold_cnt = 0u;
+        h->fold_fail = 0u;
         h->cg_gamma = 0.0;
     }
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
@@ -468,6 +519,7 @@ const char *kpl_breakdown_message(int64_t code) {
     case BD_NONPOS_SP: return "nonpositive curvature (s, p)";
     case BD_PEER_TIMEOUT: return "peer exchange timeout";
     case BD_BARRIER_TIMEOUT: return "device barrier timeout";
+    case BD_PEER_FAILED: return "peer rank failed";
     default: return "";
     }
 }
@@ -522,8 +574,11 @@ int kpl_spmv(const kpl_op *op, const double *v, double *out, void *stream) {
     if (op->kind == KPL_OP_CSR) {
         CGeo g{op->n, op->row_ptr, op->col_idx, op->values};
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        csr_spmv_kernel<InVec<KPL_PC_IDENTITY>><<<(unsigned)L.items, NT, 0, (cudaStream_t)stream>>>(
-            g, in, out, ws, PRED_ALWAYS, 0);
+        if (op->sp_col)
+            launch_sorted(op, g, in, out, ws, PRED_ALWAYS, 0, (cudaStream_t)stream);
+        else
+            csr_spmv_kernel<InVec<KPL_PC_IDENTITY>><<<(unsigned)L.items, NT, 0, (cudaStream_t)stream>>>(
+                g, in, out, ws, PRED_ALWAYS, 0);
         return cuda_check("spmv launch");
     }
     return launch(op, L, in, body, ws, cfg, PH_NONE, PRED_ALWAYS, 0, (cudaStream_t)stream);
@@ -881,21 +936,32 @@ int kpl_sweep(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int32_t 
 
 int kpl_sweep_peer(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int32_t kind, int64_t row,
                    void *workspace, const kpl_peer_sweep *px, uint64_t epoch, int32_t table_parity, int32_t push,
-                   int32_t wpar, void *stream) {
+                   int32_t wpar, uint64_t wait_epoch, int32_t wait_parity, void *stream) {
     Ctx c;
     int rc = make_ctx(op, cfgp, v, workspace, stream, c);
     if (rc != KPL_OK) return rc;
     if (!px) return fail(KPL_EINVAL, "null peer descriptor");
     if (op->kind != KPL_OP_STENCIL || kind != KPL_SW_ITER || op->chunks_global <= 0)
         return fail(KPL_EUNSUPPORTED, "fused peer exchange: multi-GPU stencil iteration sweeps only");
-    if (table_parity < 0 || table_parity > 1 || wpar < 0 || wpar > 1 || (push & ~(KPL_PUSH_W | KPL_PUSH_X)))
+    if (table_parity < 0 || table_parity > 1 || wpar < 0 || wpar > 1 || (push & ~(KPL_PUSH_W | KPL_PUSH_X)) ||
+        wait_parity < 0 || wait_parity > 1)
         return fail(KPL_EINVAL, "bad parity / push mask");
+    if (wait_epoch && (c.cfg.method == KPL_M_PCG_RR || c.cfg.track_gaps))
+        return fail(KPL_EUNSUPPORTED, "deferred fold: p-CG / p-CG-sh / p-CG-var-sh without gaps only");
     c.ws.px = px;
+    c.ws.wait_epoch = (unsigned long long)wait_epoch;
+    c.ws.wait_tpar = wait_parity;
     c.ws.epoch = (unsigned long long)epoch;
     c.ws.tpar = table_parity;
     c.ws.push = push;
     c.ws.wpar = wpar;
     return do_sweep(c, kind, row);
+}
+
+int kpl_set_peer_timeout(double seconds) {
+    if (!(seconds > 0.0) || seconds > 1e6) return fail(KPL_EINVAL, "peer timeout must be in (0, 1e6] s");
+    g_peer_timeout_ns.store((unsigned long long)(seconds * 1e9), std::memory_order_relaxed);
+    return KPL_OK;
 }
 
 int kpl_sweep_phase(int32_t kind) {

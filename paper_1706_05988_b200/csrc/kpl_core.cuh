@@ -32,7 +32,8 @@ struct WsHead {
     long long cg_last, _cg_pad;
     unsigned long long bar_arrive;                // one-phase grid barrier (persistent_redundant)
     double dsig_pad[3];
-    unsigned int final_cnt, bar_cnt, bar_gen, _cnt_pad[5];   // completion count; grid barrier
+    unsigned int final_cnt, bar_cnt, bar_gen;     // completion count; grid barrier
+    unsigned int fold_cnt, fold_fail, _cnt_pad[3];  // deferred peer fold: readers done; a failed wait
 };
 static_assert(sizeof(WsHead) <= 1024, "head too large");
 
@@ -89,6 +90,13 @@ struct Ws {                   // device view of the caller's workspace
     int tpar;                 // exchange-table slot the chunk partials go to
     int push;                 // KPL_PUSH_* outputs whose boundary planes go to the neighbours
     int wpar;                 // which ping-pong w is the output
+    // deferred fold (kpl_sweep_peer, wait_epoch != 0): every CTA first waits for
+    // the previous sweep's exchange (flags >= wait_epoch), folds table slot
+    // wait_tpar and runs its epilogue on a private copy of the head
+    unsigned long long wait_epoch;
+    int wait_tpar;
+    unsigned long long timeout_ns;   // peer waits: give up after this long
+    unsigned int *final_cnt;  // chunk-completion count (on the real head, also in a private view)
 };
 
 // Product sink of the reference-order mode: bodies accumulate through accp(),
@@ -149,16 +157,10 @@ __device__ __forceinline__ void ld_ro(const double *p, long long k, double (&o)[
 // GPU-scope load whose asm carries a "memory" clobber, so the compiler keeps
 // it after the barrier / epilogue stores that precede it in program order
 // (__ldcg's asm has no clobber, so nothing but the barrier orders it).
-__device__ __forceinline__ long long ld_head(const long long *p) {
-    long long v;
-    asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ double ld_head(const double *p) {
-    double v;
-    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-    return v;
-}
+// Generic address: the head is global memory, or a CTA's private copy in
+// shared memory (deferred peer fold).
+__device__ __forceinline__ long long ld_head(const long long *p) { return *(const volatile long long *)p; }
+__device__ __forceinline__ double ld_head(const double *p) { return *(const volatile double *)p; }
 
 // Programmatic dependent launch: sweeps may be launched while the previous
 // kernel in the stream is still draining (cudaLaunchAttributeProgrammatic-
@@ -238,7 +240,9 @@ enum Breakdown : int {
     BD_VANISH_DEN = 4,       // "vanishing alpha denominator"
     BD_NONFINITE = 5,        // "non-finite coefficients"
     BD_NONPOS_SP = 6,        // "nonpositive curvature (s, p)"
-    BD_BARRIER_TIMEOUT = 8,  // "device barrier timeout" (persistent solver; 7 = peer exchange timeout)
+    BD_PEER_TIMEOUT = 7,     // "peer exchange timeout"
+    BD_BARRIER_TIMEOUT = 8,  // "device barrier timeout" (persistent solver)
+    BD_PEER_FAILED = 9,      // "peer rank failed" (a peer signalled poison)
 };
 
 __device__ __forceinline__ void set_breakdown(WsHead *h, long long i, int code) {
@@ -438,12 +442,56 @@ __device__ __forceinline__ bool pred_ok(const WsHead *h, int pred, long long row
 }
 
 // ---------------------------------------------------- fused peer exchange
+// Flags are monotone epochs; a rank whose exchange failed (a wait timed out,
+// or a peer's poison was seen) signals epoch | PEER_POISON from then on, so
+// every peer fails its next wait at once instead of folding stale partials.
+constexpr unsigned long long PEER_POISON = 1ull << 63;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release_sys_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ bool peer_failed(const WsHead *h) {
+    if (!h || ld_head(&h->state) != KPL_ST_BREAKDOWN) return false;
+    const long long c = ld_head(&h->bd_code);
+    return c == BD_PEER_TIMEOUT || c == BD_PEER_FAILED;
+}
+__device__ __forceinline__ unsigned long long peer_signal_value(const WsHead *h, unsigned long long epoch) {
+    return epoch | (peer_failed(h) ? PEER_POISON : 0ull);
+}
+
+// Wait until flags[0..nranks) >= epoch (acquire, system scope).  Returns 0,
+// or BD_PEER_FAILED (a peer's poison) / BD_PEER_TIMEOUT.  `abort` (optional):
+// a word another CTA of this rank sets when its own wait failed.
+__device__ __noinline__ int peer_wait(const unsigned long long *flags, int nranks, unsigned long long epoch,
+                                      unsigned long long timeout_ns, const unsigned *abort) {
+    const unsigned long long t0 = globaltimer_ns();
+    for (int p = 0; p < nranks; ++p) {
+        for (;;) {
+            const unsigned long long v = ld_acquire_sys(flags + p);
+            if (v & PEER_POISON) return BD_PEER_FAILED;
+            if (v >= epoch) break;
+            __nanosleep(64);
+            if (abort && *(const volatile unsigned *)abort) return BD_PEER_FAILED;
+            if (globaltimer_ns() - t0 > timeout_ns) return BD_PEER_TIMEOUT;
+        }
+    }
+    return 0;
+}
+
 __device__ __forceinline__ void peer_signal_all(const Ws &ws) {
+    const unsigned long long v = peer_signal_value(ws.head, ws.epoch);
     for (int p = 0; p < ws.px->nranks; ++p)
-        st_release_sys_u64(reinterpret_cast<unsigned long long *>(ws.px->signal[p]), ws.epoch);
+        st_release_sys_u64(reinterpret_cast<unsigned long long *>(ws.px->signal[p]), v);
 }
 
 // A predicated-off fused sweep still signals (the finalize skips its fold by
@@ -453,6 +501,83 @@ __device__ __forceinline__ void peer_signal_idle(const Ws &ws) {
         __threadfence_system();
         peer_signal_all(ws);
     }
+}
+
+// ---- deferred fold: the reduction exchange of sweep i-1 folded inside sweep i
+// (the paper's overlap: no finalize launch between sweeps).
+struct FoldSmem {
+    WsHead head;              // this CTA's private copy of the head (epilogue applied)
+    double row[HC];           // its history row (scratch)
+};
+
+// The view every later part of the sweep uses: scalars from `h` (the private
+// head) and history into `row`; counters stay on the real head.  Built field
+// by field (see ws_view in kpl_sweep.cuh for why).
+__device__ __forceinline__ Ws ws_fold_view(const Ws &ws, WsHead *h, double *row, bool fold) {
+    Ws w;
+    w.head = fold ? h : ws.head; w.items = ws.items; w.chunks = ws.chunks; w.chunk_cnt = ws.chunk_cnt;
+    w.hist = fold ? row : ws.hist; w.reps = ws.reps; w.nbuf = ws.nbuf; w.mbuf = ws.mbuf;
+    w.chunk_offset = ws.chunk_offset; w.chunks_global = ws.chunks_global; w.inline_final = ws.inline_final;
+    w.prod = ws.prod; w.nprod = ws.nprod; w.hist_scratch = fold ? 1 : ws.hist_scratch;
+    w.px = ws.px; w.epoch = ws.epoch; w.tpar = ws.tpar; w.push = ws.push; w.wpar = ws.wpar;
+    w.wait_epoch = ws.wait_epoch; w.wait_tpar = ws.wait_tpar; w.timeout_ns = ws.timeout_ns;
+    w.final_cnt = ws.final_cnt;
+    return w;
+}
+
+// Every CTA (all threads): wait for every rank's flag of the previous sweep,
+// copy the head, fold this rank's table slot (the level-4 tree of a single
+// GPU: strided_sum over chunks_global, as peer_finalize_kernel) and run the
+// pipelined epilogue on the copy -- every CTA computes the same alpha_i,
+// beta_i bit for bit.  The last CTA to finish reading the real head publishes
+// its copy (scalars + history row) there.  Only for PH_PIPE sweeps that
+// follow a fused iteration sweep of the same solve (the host decides).
+__device__ __noinline__ void peer_fold_start(const Ws &ws, const Cfg &cfg, FoldSmem &fs, double *sred) {
+    __shared__ int s_fail;
+    if (threadIdx.x == 0)       // nothing to wait for once the solve has stopped
+        s_fail = ld_head(&ws.head->state) != KPL_ST_RUNNING
+                     ? 0 : peer_wait(reinterpret_cast<const unsigned long long *>(ws.px->flags), ws.px->nranks, ws.wait_epoch, ws.timeout_ns, &ws.head->fold_fail);
+    {
+        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(ws.head);
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(&fs.head);
+        for (int k = threadIdx.x; k < (int)(sizeof(WsHead) / 8); k += blockDim.x) dst[k] = __ldcg(src + k);
+    }
+    if (threadIdx.x == 0) __threadfence_system();
+    __syncthreads();
+    const bool running = fs.head.state == KPL_ST_RUNNING;   // the finalize's PRED_RUNNING
+    double f[NQ];
+    strided_sum<NQ>(ws.px->table[ws.wait_tpar][ws.px->rank], ws.chunks_global, NQ, f, sred);
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < HC; ++c) fs.row[c] = __longlong_as_double(0x7ff8000000000000LL);
+        const Ws v = ws_fold_view(ws, &fs.head, fs.row, true);
+        if (s_fail) {
+            if (running) set_breakdown(&fs.head, -1, s_fail);
+            atomicOr(&ws.head->fold_fail, 1u << s_fail);
+        } else if (running) {
+            finalize(v, cfg, PH_PIPE, f);
+        }
+        __threadfence();
+        const unsigned prev = atomicAdd(&ws.head->fold_cnt, 1u);
+        if (prev == gridDim.x - 1) {               // every CTA has read the real head
+            __threadfence();
+            const unsigned fail = atomicExch(&ws.head->fold_fail, 0u);
+            WsHead *h = ws.head;
+            if (fail && running && fs.head.state != KPL_ST_BREAKDOWN)
+                set_breakdown(&fs.head, -1, (fail >> BD_PEER_FAILED) & 1 ? BD_PEER_FAILED : BD_PEER_TIMEOUT);
+            // scalars only: the counters (from bar_arrive on) belong to running sweeps
+            const size_t nsc = offsetof(WsHead, bar_arrive) / 8;
+            const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&fs.head);
+            unsigned long long *dst = reinterpret_cast<unsigned long long *>(h);
+            for (size_t k = 0; k < nsc; ++k) dst[k] = src[k];
+            if (running && !s_fail && fs.head.state != KPL_ST_BREAKDOWN) {
+                double *row = ws.hist + HC * fs.head.iter;
+                for (int c = 0; c < 5; ++c) row[c] = fs.row[c];
+            }
+            h->fold_cnt = 0u;
+            __threadfence();
+        }
+    }
+    __syncthreads();
 }
 
 // Halo part of the fused exchange: CTAs of the slab's first / last chunk copy
@@ -525,9 +650,9 @@ __device__ void complete_item(const Ws &ws, const Cfg &cfg, const Layout &L, int
                 for (int q = 0; q < NQ; ++q) dst[q] = q < Q ? v[q] : 0.0;
             }
             __threadfence_system();
-            const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
+            const unsigned prev = atomicAdd(ws.final_cnt, 1u);
             if (prev == (unsigned)(L.nch - 1)) {
-                ws.head->final_cnt = 0u;
+                *ws.final_cnt = 0u;
                 __threadfence_system();
                 peer_signal_all(ws);
             }
@@ -536,7 +661,7 @@ __device__ void complete_item(const Ws &ws, const Cfg &cfg, const Layout &L, int
     if (!ws.inline_final) return;
     if (threadIdx.x == 0) {
         __threadfence();
-        const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
+        const unsigned prev = atomicAdd(ws.final_cnt, 1u);
         s_last = (prev == (unsigned)(L.nch - 1));
         if (s_last) __threadfence();
     }
@@ -549,7 +674,7 @@ __device__ void complete_item(const Ws &ws, const Cfg &cfg, const Layout &L, int
 #pragma unroll
         for (int q = 0; q < Q; ++q) full[q] = f[q];
         finalize(ws, cfg, phase, full);
-        ws.head->final_cnt = 0u;
+        *ws.final_cnt = 0u;
         __threadfence();
     }
 }

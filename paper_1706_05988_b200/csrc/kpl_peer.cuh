@@ -24,23 +24,6 @@
 
 namespace kpl {
 
-constexpr int BD_PEER_TIMEOUT = 7;                       // "peer exchange timeout"
-constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
-
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 // Copies (grid-stride over every copy in turn), then the completion count and
 // the signals.  `cnt` is a device word of this rank, zero before the first
 // post; atomicInc wraps it back to zero in the last CTA.
@@ -65,8 +48,10 @@ __global__ void __launch_bounds__(NT) peer_post_kernel(kpl_post post, unsigned l
     }
     __syncthreads();
     if (!s_last) return;
+    // a rank whose exchange failed signals poison, so no peer folds stale partials
+    const unsigned long long v = peer_signal_value(reinterpret_cast<const WsHead *>(post.status), epoch);
     for (int p = threadIdx.x; p < post.nsignals; p += blockDim.x)
-        st_release_sys(reinterpret_cast<unsigned long long *>(post.signal[p]), epoch);
+        st_release_sys_u64(reinterpret_cast<unsigned long long *>(post.signal[p]), v);
 }
 
 // Wait for every rank's flag >= epoch, then (reducing sweeps) fold the
@@ -77,18 +62,12 @@ __global__ void __launch_bounds__(NT) peer_finalize_kernel(Ws ws, Cfg cfg, int p
     __shared__ double sred[NQ * NWARP];
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
-        // after one timeout the exchange is dead: later waits return at once
-        int ok = !(ws.head && ws.head->state == KPL_ST_BREAKDOWN && ws.head->bd_code == BD_PEER_TIMEOUT);
-        const unsigned long long t0 = globaltimer_ns();
-        for (int p = 0; p < nranks && ok; ++p) {
-            while (ld_acquire_sys(flags + p) < epoch) {
-                __nanosleep(64);
-                if (globaltimer_ns() - t0 > kPeerTimeoutNs) { ok = 0; break; }
-            }
-        }
-        if (!ok && ws.head && ws.head->state == KPL_ST_RUNNING) set_breakdown(ws.head, -1, BD_PEER_TIMEOUT);
+        // after a failure the exchange is dead: later waits return at once (and
+        // this rank's posts signal poison from now on)
+        int code = peer_failed(ws.head) ? BD_PEER_FAILED : peer_wait(flags, nranks, epoch, ws.timeout_ns, nullptr);
+        if (code && ws.head && ws.head->state == KPL_ST_RUNNING) set_breakdown(ws.head, -1, code);
         __threadfence_system();
-        s_ok = ok;
+        s_ok = code == 0;
     }
     __syncthreads();
     if (!s_ok || phase == PH_NONE || !ws.head) return;

@@ -225,11 +225,15 @@ __device__ __forceinline__ void stencil_pass(const SGeo &g, const Layout &L, In 
 
 template <int VX, class In, class Body>
 __global__ void __launch_bounds__(NT, 2)
-stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
+stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws_in, Cfg cfg, int phase, int pred, long long row) {
     __shared__ __align__(16) double sp[Body::kStencil ? 2 * SMEM_PLANE : 2];
     __shared__ double sred[NQ * NWARP];
+    __shared__ FoldSmem fsm;
     pdl_wait();
     pdl_launch_dependents();
+    const bool fold = ws_in.px && ws_in.wait_epoch;
+    if (fold) peer_fold_start(ws_in, cfg, fsm, sred);      // deferred fold of the previous sweep
+    const Ws ws = ws_fold_view(ws_in, &fsm.head, fsm.row, fold);
     if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
     stencil_pass<VX, In, Body>(g, L, in, body, ws, cfg, phase, sp, sred);
 }
@@ -391,6 +395,7 @@ __device__ __forceinline__ Ws ws_view(const Ws &ws, WsHead *head, double *hist, 
     w.reps = ws.reps; w.nbuf = ws.nbuf; w.mbuf = ws.mbuf; w.chunk_offset = ws.chunk_offset;
     w.chunks_global = ws.chunks_global; w.inline_final = ws.inline_final; w.prod = ws.prod; w.nprod = ws.nprod;
     w.hist_scratch = scratch; w.px = nullptr; w.epoch = 0; w.tpar = 0; w.push = 0; w.wpar = 0;
+    w.wait_epoch = 0; w.wait_tpar = 0; w.timeout_ns = ws.timeout_ns; w.final_cnt = ws.final_cnt;
     return w;
 }
 
@@ -504,6 +509,86 @@ csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long l
     }
 }
 
+// Column-sorted gather form of csr_spmv_kernel (kpl_op.sp_*; scattered
+// matrices such as config 5's random band, where a CSR-order warp gather
+// touches ~31 cache lines and the SpMV is bound by L1 wavefronts).  One CTA
+// per block of S.R rows: phase 1 streams the block's nonzeros in column order
+// (coalesced col/val/dest, gathers whose lanes share lines: ~9 lines per warp
+// at 1024 rows) and stores each product at its CSR position in shared memory;
+// phase 2 sums every row left to right from +0.0 out of shared memory -- the
+// csr_matvec order, so n is bit-identical to csr_spmv_kernel's.
+struct SGather {
+    const int *col;
+    const double *val;
+    const unsigned short *dest;
+    int R;                    // rows per block
+};
+
+template <class In, int NTS, int PER, bool L2G = false>
+__global__ void __launch_bounds__(NTS, 1)
+csr_sorted_spmv(CGeo g, SGather S, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
+    extern __shared__ double sprod[];
+    pdl_wait();
+    pdl_launch_dependents();
+    if (ws.head && !pred_ok(ws.head, pred, row)) return;
+    if (ws.head) in.setup(ws);
+    const int tid = threadIdx.x;
+    const long long nblk = (g.n + S.R - 1) / S.R;
+    const double *base = in.base();
+    constexpr long long STEP = (long long)NTS * PER;
+    // software pipeline: the (col, val, dest) stream of round k+1 -- or of the
+    // next block's first round -- is in flight while round k's gathers are
+    int col[PER], d[PER], ncol[PER], nd[PER];
+    double val[PER], nval[PER];
+    auto fetch = [&](long long kb, long long k1, int (&c)[PER], double (&v)[PER], int (&dd)[PER]) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const long long kk = kb + (long long)j * NTS;
+            c[j] = 0; dd[j] = 0; v[j] = 0.0;
+            if (kk < k1) { c[j] = __ldcs(S.col + kk); v[j] = __ldcs(S.val + kk); dd[j] = __ldcs(S.dest + kk); }
+        }
+    };
+    long long blk = blockIdx.x;
+    long long k0 = 0, k1 = 0;
+    if (blk < nblk) {
+        k0 = __ldg(g.row_ptr + blk * S.R);
+        k1 = __ldg(g.row_ptr + min(blk * S.R + S.R, g.n));
+        fetch(k0 + tid, k1, col, val, d);
+    }
+    for (; blk < nblk; blk += gridDim.x) {
+        const long long r0 = blk * S.R, r1 = min(r0 + (long long)S.R, g.n);
+        const long long nb = blk + gridDim.x;
+        long long nk0 = 0, nk1 = 0;
+        if (nb < nblk) { nk0 = __ldg(g.row_ptr + nb * S.R); nk1 = __ldg(g.row_ptr + min(nb * S.R + S.R, g.n)); }
+        for (long long kb = k0 + tid; kb < k1; kb += STEP) {
+            const bool more = kb + STEP < k1;
+            if (more) fetch(kb + STEP, k1, ncol, nval, nd);
+            else if (nb < nblk) fetch(nk0 + tid, nk1, ncol, nval, nd);      // next block's first round
+            double raw[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                raw[j] = 0.0;
+                if (kb + (long long)j * NTS < k1) raw[j] = load1<L2G>(in, base, col[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < PER; ++j)
+                if (kb + (long long)j * NTS < k1) sprod[d[j]] = __dmul_rn(val[j], in.xf(raw[j], col[j]));
+#pragma unroll
+            for (int j = 0; j < PER; ++j) { col[j] = ncol[j]; val[j] = nval[j]; d[j] = nd[j]; }
+        }
+        if (k0 + tid >= k1 && nb < nblk) fetch(nk0 + tid, nk1, col, val, d);  // no round this block
+        __syncthreads();
+        for (long long r = r0 + tid; r < r1; r += NTS) {
+            const int a0 = __ldg(g.row_ptr + r) - (int)k0, a1 = __ldg(g.row_ptr + r + 1) - (int)k0;
+            double a = 0.0;
+            for (int kk = a0; kk < a1; ++kk) a = __dadd_rn(a, sprod[kk]);   // csr_matvec order
+            out[r] = a;
+        }
+        __syncthreads();
+        k0 = nk0; k1 = nk1;
+    }
+}
+
 template <class In, class Body, bool L2G = false>
 __global__ void __launch_bounds__(NT, 3)
 csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ nin, Ws ws, Cfg cfg, int phase,
@@ -573,7 +658,7 @@ csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ n
         if (ws.inline_final) {
             if (tid == 0) {
                 __threadfence();
-                const unsigned prev = atomicAdd(&ws.head->final_cnt, 1u);
+                const unsigned prev = atomicAdd(ws.final_cnt, 1u);
                 s_last = (prev == (unsigned)(L.nch - 1));
                 if (s_last) __threadfence();
             }
@@ -586,7 +671,7 @@ csr_chunk_sweep(CGeo g, Layout L, In in, Body body, const double *__restrict__ n
 #pragma unroll
                     for (int q = 0; q < Q; ++q) full[q] = f[q];
                     finalize(ws, cfg, phase, full);
-                    ws.head->final_cnt = 0u;
+                    *ws.final_cnt = 0u;
                     __threadfence();
                 }
             }

@@ -105,7 +105,7 @@ struct TmaRing {
 // Jacobi (m = w * cin, precond.py:88-89 with inv_diag == cin).
 template <class Body, int D, int PCIN = 0, bool TWO_D = false>
 __global__ void __launch_bounds__(NT + 32, 2)
-tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws ws, Cfg cfg, int phase,
+tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws ws_in, Cfg cfg, int phase,
           int pred, long long row, int wsel, int wzoff, double cin) {
     using S = TmaShape<TWO_D>;
     constexpr int NSTR = Body::kTmaStreams;
@@ -122,9 +122,13 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
     unsigned long long *wempty = sfull + SS;
     unsigned long long *sempty = wempty + SW;
     __shared__ double sred[NQ * NWARP];
+    __shared__ FoldSmem fsm;
 
     pdl_wait();
     pdl_launch_dependents();
+    const bool fold = ws_in.px && ws_in.wait_epoch;
+    if (fold) peer_fold_start(ws_in, cfg, fsm, sred);      // deferred fold of the previous sweep
+    const Ws ws = ws_fold_view(ws_in, &fsm.head, fsm.row, fold);
     if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
     body.setup(ws);
     const long long par = wsel ? (ws.head->iter & 1) : 0;    // w_in = w[iter & 1] (ping-pong) or fixed

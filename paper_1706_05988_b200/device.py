@@ -96,11 +96,14 @@ class DeviceMatrix:
     def __init__(self, A, device):
         t = torch()
         self.n = int(A.n)
+        self.device = t.device(device)
+        self.stamp = _matrix_stamp(A)
         if hasattr(A, "stencil_spec"):
             self.kind = _lib.KPL_OP_STENCIL
             self.nx, self.ny, self.nz, self.diag = A.stencil_spec()
             self.row_ptr = self.col_idx = self.values = None
             self.nnz = 0
+            self.sorted = None
         else:
             self.kind = _lib.KPL_OP_CSR
             nnz = len(A.values)
@@ -112,15 +115,83 @@ class DeviceMatrix:
             self.nnz = nnz
             self.nx = self.ny = self.nz = 0
             self.diag = 0.0
+            self.sorted = sorted_gather_layout(A.row_ptr, A.col_idx, self.row_ptr, self.col_idx, self.values)
+
+
+# Column-sorted SpMV gathers (kpl_op.sp_*): worth it when a CSR-order warp
+# gather touches many cache lines (config 5's random band: ~31 of 32 lanes on
+# distinct 128-byte lines; a 7-point stencil matrix: ~6).  KPL_CSR_GATHER =
+# auto (default) | csr | sorted.
+_SORTED_MIN_LINES = 12.0
+_SORTED_MAX_NNZ = 27 * 1024            # products per block in shared memory (216 KiB)
+
+
+def csr_lines_per_warp(col_idx, sample=1 << 16):
+    """Mean distinct 128-byte lines of the input a 32-lane CSR-order gather touches
+    (first `sample` nonzeros)."""
+    c = np.asarray(col_idx[:sample], dtype=np.int64) // 16
+    m = len(c) - len(c) % 32
+    if m == 0:
+        return 0.0
+    w = np.sort(c[:m].reshape(-1, 32), axis=1)
+    return float(1.0 + (np.diff(w, axis=1) != 0).sum(axis=1).mean())
+
+
+def sorted_gather_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values):
+    """(sp_col, sp_val, sp_dest, rows per block, max block nnz) or None.  Index
+    work only (the values are permuted, never combined), done once per matrix
+    with device sorts."""
+    mode = os.environ.get("KPL_CSR_GATHER", "auto")
+    if mode not in ("auto", "csr", "sorted"):
+        raise ValueError(f"KPL_CSR_GATHER={mode!r}: expected auto, csr or sorted")
+    if mode == "csr" or (mode == "auto" and csr_lines_per_warp(col_idx_h) < _SORTED_MIN_LINES):
+        return None
+    rp = np.asarray(row_ptr_h, dtype=np.int64)
+    n = len(rp) - 1
+    R = 0
+    for cand in (1024, 512, 256, 128, 64, 32):
+        ends = np.minimum(np.arange(0, n, cand) + cand, n)
+        most = int((rp[ends] - rp[np.arange(0, n, cand)]).max()) if n else 0
+        if most <= _SORTED_MAX_NNZ:
+            R = cand
+            break
+    if R == 0 or most < 1:
+        return None
+    t = torch()
+    counts = (row_ptr[1:] - row_ptr[:-1]).long()
+    blk = t.repeat_interleave(t.arange(n, device=row_ptr.device) // R, counts)
+    perm = t.argsort(blk * (1 << 31) + col_idx.long())
+    del counts
+    sp_col = col_idx[perm].contiguous()
+    sp_val = values[perm].contiguous()
+    first = row_ptr.long()[blk[perm] * R]
+    sp_dest = (perm - first).to(t.int32).to(t.int16).contiguous()     # < 65536: uint16 bits
+    del blk, perm, first
+    return sp_col, sp_val, sp_dest, R, most
+
+
+def _matrix_stamp(A):
+    """What a cached upload must still match: the host arrays' identity and
+    size (a matrix whose arrays were replaced, or resized, is re-uploaded)."""
+    if hasattr(A, "stencil_spec"):
+        return ("stencil",) + tuple(A.stencil_spec())
+    v = A.values
+    return ("csr", int(A.n), len(v), id(v), id(A.col_idx), id(A.row_ptr))
+
+
+def _fresh(dm, device):
+    """A cached device copy is usable only on the device it lives on and for
+    the host arrays it was made from (keyed on the device)."""
+    return dm is not None and dm.device == torch().device(device)
 
 
 def device_matrix(A, device) -> DeviceMatrix:
     cached = getattr(A, "_device", None) if _has_slot(A) else None
-    if cached is not None:
+    if _fresh(cached, device) and cached.stamp == _matrix_stamp(A):
         return cached
     if not _has_slot(A):
         hit = _foreign_cache.get(id(A))
-        if hit is not None and hit[0] is A:
+        if hit is not None and hit[0] is A and _fresh(hit[1], device) and hit[1].stamp == _matrix_stamp(A):
             return hit[1]
     dm = DeviceMatrix(A, device)
     if _has_slot(A):
@@ -168,10 +239,16 @@ class DevicePrecond:
         elif kind == "ic0":
             if dm.kind != _lib.KPL_OP_CSR:
                 raise NotImplementedError("IC(0) runs with CSR operators (use A.to_csr())")
-            if M.ic.n != dm.n:
+            ic = getattr(M, "ic", None)
+            if ic is None:
+                # a reference kpl.make_ic0 object: host factor in _l, its transpose in _lt
+                # (precond.py:64-70, :134-154) -> uploaded as they are
+                from .precond import ic0_from_host
+                ic = ic0_from_host(M._l, M._lt, device)
+            if ic.n != dm.n:
                 raise ValueError("dimension mismatch in preconditioner apply")
             self.code = _lib.KPL_PC_IC0
-            self.ic = M.ic
+            self.ic = ic
         else:
             raise NotImplementedError(f"preconditioner kind {kind!r} is not on the device path")
 
@@ -186,18 +263,21 @@ _pc_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 def device_precond(M, dm, device) -> DevicePrecond:
     if M is None or getattr(M, "kind", "identity") == "identity":
         return DevicePrecond(None, dm, device)
-    key = (id(dm),)
+    key = (id(dm), str(torch().device(device)))
     try:
         hit = _pc_cache.get(M)
-    except TypeError:
-        hit = None
+    except TypeError:            # reference Preconditioner: __slots__, not weak-referenceable
+        hit = _foreign_cache.get(("pc", id(M)))
+        hit = hit[1:] if hit is not None and hit[0] is M else None
     if hit is not None and hit[0] == key:
         return hit[1]
     dp = DevicePrecond(M, dm, device)
     try:
         _pc_cache[M] = (key, dp)
     except TypeError:
-        pass
+        if len(_foreign_cache) >= _FOREIGN_MAX:
+            _foreign_cache.pop(next(iter(_foreign_cache)))
+        _foreign_cache[("pc", id(M))] = (M, key, dp)
     return dp
 
 
@@ -217,6 +297,10 @@ def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk
         op.col_idx = ptr(dm.col_idx)
         op.values = ptr(dm.values)
         op.nnz = dm.nnz
+        if dm.sorted is not None:
+            sc, sv, sd, R, most = dm.sorted
+            op.sp_col, op.sp_val, op.sp_dest = ptr(sc), ptr(sv), ptr(sd)
+            op.sp_rows, op.sp_max = R, most
     op.zc = zc
     op.vx = vx
     op.chunk_blocks = chunk_blocks

@@ -36,6 +36,7 @@ track_gaps.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -178,22 +179,27 @@ class _RankState:
         self.reps_off = lib.kpl_replacements_offset(op, cfg.max_iters)
         self.status = _lib.KplStatus()
 
-    # -- device calls
+    # -- device calls (on this rank's stream: the current stream, or its own
+    #    stream when a LocalPeerComm runs the ranks concurrently)
+    stream = None
+
+    def hs(self):
+        return self.stream.cuda_stream if self.stream is not None else D.stream_handle()
+
     def prepare(self):
         _lib.check(_lib.load().kpl_solver_prepare(self.op, self.kcfg, self.vecs, D.ptr(self.ws),
-                                                  D.stream_handle()), "prepare")
+                                                  self.hs()), "prepare")
 
     def sweep(self, kind, row=0):
         _lib.check(_lib.load().kpl_sweep(self.op, self.kcfg, self.vecs, kind, row, D.ptr(self.ws),
-                                         D.stream_handle()), f"sweep {kind}")
+                                         self.hs()), f"sweep {kind}")
 
     def finalize(self, kind, row=0):
         _lib.check(_lib.load().kpl_finalize_global(self.op, self.kcfg, kind, row, D.ptr(self.ws),
-                                                   D.stream_handle()), f"finalize {kind}")
+                                                   self.hs()), f"finalize {kind}")
 
     def read_status(self):
-        _lib.check(_lib.load().kpl_read_status(D.ptr(self.ws), self.status, D.stream_handle()),
-                   "status")
+        _lib.check(_lib.load().kpl_read_status(D.ptr(self.ws), self.status, self.hs()), "status")
         return self.status
 
     def history(self, rows):
@@ -350,6 +356,9 @@ class LocalComm:
     def local_ranks(self):
         return list(range(self.size))
 
+    def solve_barrier(self):
+        pass
+
     def exchange(self, states, name):
         for s in states:
             r = s.rank
@@ -381,7 +390,7 @@ class TorchComm:
         self.group = group
         self.size = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self._counts = None
+        self._counts = {}          # per partition plan: every rank's chunk count
         # gloo moves CUDA tensors for collectives but not point-to-point: stage
         # those through host memory (used to run the multi-process path on a
         # single GPU; NCCL is the production backend)
@@ -410,6 +419,12 @@ class TorchComm:
     def local_ranks(self):
         return [self.rank]
 
+    def solve_barrier(self):
+        """Host barrier at the start of every solve: a reused peer
+        region must not receive pushes from a rank that is already in the
+        next solve while this rank is still zeroing its state."""
+        self.dist.barrier(group=self.group)
+
     def exchange(self, states, name):
         (s,) = states
         sends, recvs = [], []
@@ -432,13 +447,14 @@ class TorchComm:
     def allgather(self, states):
         (s,) = states
         t = D.torch()
-        if self._counts is None:
+        key = (s.chunk_offset, s.chunks_local, int(s.table.numel()) // 4)
+        counts = self._counts.get(key)
+        if counts is None:          # a new partition (never reuse another plan's counts)
             dev = "cpu" if self.stage_p2p else s.table.device
             c = t.tensor([s.chunks_local], dtype=t.int64, device=dev)
             allc = [t.zeros_like(c) for _ in range(self.size)]
             self.dist.all_gather(allc, c, group=self.group)
-            self._counts = [int(v.item()) for v in allc]
-        counts = self._counts
+            counts = self._counts[key] = [int(v.item()) for v in allc]
         if self.stage_p2p:                       # gloo: host-staged, equal-size (padded) all-gather
             mx = max(counts)
             mine = t.zeros(4 * mx, dtype=t.float64)
@@ -500,15 +516,20 @@ class _Regions:
 class LocalPeerComm(LocalComm):
     """P ranks on one device exchanging through the device-initiated peer path
     (kpl_peer_post / kpl_peer_finalize) with plain device pointers as the peer
-    pointers.  Every rank's sweep, post and finalize are launched in rank
-    order on one stream, so each wait is already satisfied when its kernel
-    starts (no kernel depends on another running concurrently)."""
+    pointers.  By default every rank's sweep, post and finalize are launched
+    in rank order on one stream, so each wait is already satisfied when its
+    kernel starts.  `concurrent=True` gives every rank its own CUDA stream:
+    the ranks' kernels then run at the same time and the flag waits really
+    block -- only for problems whose grids are co-resident
+    on the one device (a waiting CTA must not starve the kernel it waits for)."""
 
     peer = True
 
-    def __init__(self, P, fused=True):
+    def __init__(self, P, fused=True, concurrent=False, fold=True):
         super().__init__(P)
         self.fused = fused
+        self.fold = fold
+        self.concurrent = concurrent
         self._cache = {}
 
     def regions(self, sizes, device):
@@ -518,6 +539,12 @@ class LocalPeerComm(LocalComm):
             tens = {q: t.zeros(sz, dtype=t.uint8, device=device) for q, sz in enumerate(sizes)}
             self._cache = {key: _Regions(tens, [tens[q].data_ptr() for q in range(len(sizes))])}
         return self._cache[key]
+
+
+def LocalPeerCommNoFold(P):
+    """LocalPeerComm with a kpl_peer_finalize launch between consecutive fused
+    iteration sweeps (no deferred fold) -- the parity tests run both forms."""
+    return LocalPeerComm(P, fold=False)
 
 
 def LocalPeerCommPostOnly(P):
@@ -629,11 +656,17 @@ class DistributedSolve:
         self.peer = bool(getattr(self.comm, "peer", False))
         self._pending = None
         self.fused = False
+        self.fold = False
         if not self.peer:
             return
         # fused exchange inside the iteration sweep: stencil slabs, pipelined methods
         self.fused = (bool(getattr(self.comm, "fused", True)) and isinstance(self.plan, SlabPlan)
                       and cfg.method != "cg")
+        # ... and the deferred fold of one iteration sweep's exchange inside the next
+        # (KPL_PEER_FOLD=0 keeps a kpl_peer_finalize launch between them)
+        self.fold = (self.fused and cfg.method in ("pcg", "pcg_sh", "pcg_var_sh") and not cfg.track_gaps
+                     and bool(getattr(self.comm, "fold", True))
+                     and os.environ.get("KPL_PEER_FOLD", "1") != "0")
         if self.comm.size > _lib.KPL_PEER_MAX_RANKS:
             raise ValueError(f"peer exchange supports up to {_lib.KPL_PEER_MAX_RANKS} ranks")
         self._names = storage_names(cfg, ident)
@@ -665,6 +698,8 @@ class DistributedSolve:
         sxy, n = self.plan.sxy, self.plan.n_local
         px = _lib.KplPeerSweep()
         px.nranks = P
+        px.rank = r
+        px.flags = self.reg.bases[r] + PeerLayout.FLAGS
         for par in (0, 1):
             for q in range(P):
                 px.table[par][q] = self.reg.bases[q] + self.layouts[q].table_slot(par)
@@ -726,6 +761,7 @@ class DistributedSolve:
         for q in range(P):
             post.signal[q] = self.reg.bases[q] + PeerLayout.FLAGS + 8 * s.rank
         post.counter = self.reg.bases[s.rank] + PeerLayout.COUNTER
+        post.status = D.ptr(s.ws)            # this rank's head: poison once its exchange failed
         self._posts[key] = post
         return post
 
@@ -744,7 +780,6 @@ class DistributedSolve:
         kind, row, e, par = self._pending if self._pending is not None else (0, 0, None, 0)
         lib = _lib.load()
         reducing = kind != 0 and lib.kpl_sweep_phase(kind) != 0
-        hs = D.stream_handle()
         if e is None or push:
             # a post kernel: the halos, plus the partials unless the sweep pushed them itself
             partials = reducing and e is None
@@ -754,14 +789,14 @@ class DistributedSolve:
             self.reg.epoch += 1
             e = self.reg.epoch
             for s in self.states:
-                _lib.check(lib.kpl_peer_post(self._post_struct(s, tuple(push), partials, par), e, hs),
+                _lib.check(lib.kpl_peer_post(self._post_struct(s, tuple(push), partials, par), e, s.hs()),
                            "peer post")
         for s in self.states:
             L = self.layouts[s.rank]
             table = self.reg.bases[s.rank] + L.table_slot(par)
             _lib.check(lib.kpl_peer_finalize(s.op, s.kcfg, kind, row, D.ptr(s.ws), table,
-                                             self.reg.bases[s.rank] + PeerLayout.FLAGS, self.comm.size, e, hs),
-                       "peer finalize")
+                                             self.reg.bases[s.rank] + PeerLayout.FLAGS, self.comm.size, e,
+                                             s.hs()), "peer finalize")
         self._dirty.difference_update(push)
         self._pending = None
 
@@ -778,9 +813,27 @@ class DistributedSolve:
     def exchange(self, name):
         self.comm.exchange(self.states, name)
 
+    def _can_fold(self, kind, inputs):
+        """The deferred fold (kpl_sweep_peer wait_epoch): the pending sweep is a
+        fused iteration sweep whose exchange has not been finalised, this sweep
+        is the next fused iteration sweep, and it needs no halo push first --
+        then its CTAs fold the previous exchange themselves and no finalize
+        launch sits between the two sweeps."""
+        if not (self.fold and kind == _lib.KPL_SW_ITER and self._pending is not None):
+            return False
+        pk, _, pe, _ = self._pending
+        if pk != _lib.KPL_SW_ITER or pe is None:
+            return False
+        return not any(self.states[0].alias[nm] in self._dirty for nm in inputs)
+
     def sweep(self, kind, row=0, inputs=(), push_x=False):
         if self.peer:
-            self._flush(inputs)
+            wait_e = wait_par = 0
+            if self.fused and self._can_fold(kind, inputs):
+                _, _, wait_e, wait_par = self._pending
+                self._pending = None
+            else:
+                self._flush(inputs)
             kept = {self.states[0].alias[nm] for nm in inputs}
             if self.fused and kind == _lib.KPL_SW_ITER:
                 # the sweep pushes its w output (and x for the next cadence record)
@@ -790,11 +843,12 @@ class DistributedSolve:
                 e, par = self.reg.epoch, self.reg.red & 1
                 wout = "w0" if inputs[0] == "w1" else "w1"
                 push = _lib.KPL_PUSH_W | (_lib.KPL_PUSH_X if push_x else 0)
-                lib, hs = _lib.load(), D.stream_handle()
+                lib = _lib.load()
                 for s in self.states:
                     pxd = self.reg.bases[s.rank] + self.layouts[s.rank].px
                     _lib.check(lib.kpl_sweep_peer(s.op, s.kcfg, s.vecs, kind, row, D.ptr(s.ws), pxd, e, par, push,
-                                                  1 if wout == "w1" else 0, hs), "fused sweep")
+                                                  1 if wout == "w1" else 0, wait_e, wait_par, s.hs()),
+                               "fused sweep")
                 clean = {wout} | ({"x"} if push_x else set())
                 self._dirty.update(nm for nm in self._names if nm not in kept)
                 self._dirty.difference_update(clean)
@@ -827,6 +881,15 @@ class DistributedSolve:
 
     def init(self):
         m = self.cfg.method
+        if self.peer:
+            self.comm.solve_barrier()
+        if getattr(self.comm, "concurrent", False):
+            t = D.torch()
+            cur = t.cuda.current_stream()
+            for s in self.states:
+                if s.stream is None:
+                    s.stream = t.cuda.Stream(device=self.device)
+                s.stream.wait_stream(cur)          # setup, regions and rhs copies come first
         self._all(lambda s: s.prepare())
         if self.peer:
             self._pending = (0, 0, None, 0)    # barrier: no peer pushes into this rank before its prepare
@@ -877,6 +940,13 @@ class DistributedSolve:
             st = self._status()
         return self.result()
 
+    def _join(self):
+        """The current stream waits for every rank stream (concurrent ranks)."""
+        cur = D.torch().cuda.current_stream()
+        for s in self.states:
+            if s.stream is not None:
+                cur.wait_stream(s.stream)
+
     def result(self):
         s0 = self.states[0]
         st = self._status()
@@ -897,6 +967,7 @@ class DistributedSolve:
             self.record(int(st.iter), cadence_only=False)
             if self.peer:
                 self._flush()
+        self._join()
         history = records_from(s0.history(rows), rows)
         reps = []
         if st.n_replacements:

@@ -137,6 +137,24 @@ class Ic0Factor:
         return ptr, col, self.l_val.cpu().numpy()
 
 
+def ic0_from_host(lower, upper, device):
+    """Upload a host IC(0) factor as the reference stores it (precond.py:64-70):
+    `lower` = (row_ptr, col_idx, values) of L, diagonal last per row; `upper` =
+    its transpose from _transpose_csr (precond.py:46-53), diagonal first.  No
+    arithmetic: the factor values are the reference's own."""
+    from . import device as D
+    t = D.torch()
+    ptr, cols, lval = (np.asarray(a) for a in lower)
+    tptr, tcols, uval = (np.asarray(a) for a in upper)
+    n = len(ptr) - 1
+    if len(cols) >= 2**31:
+        raise ValueError("factor too large for int32 indices")
+    i32 = lambda a: t.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)
+    f64 = lambda a: t.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
+    return Ic0Factor(n, i32(ptr), i32(cols), f64(lval), i32(tptr), i32(tcols), f64(uval),
+                     np.asarray(ptr, dtype=np.int64), np.asarray(cols, dtype=np.int64))
+
+
 def _lower_pattern(A):
     """precond.py:28-43 index part: the lower triangle's row pointer, columns
     and the positions of its entries in A.values (diagonal last per row)."""

@@ -133,7 +133,7 @@ def _one_gpu(A, M, b, cfg, zc):
     return _Solve(A, M, b, None, cfg, zc=zc, slab_view=True).run()
 
 
-COMMS = ["LocalComm", "LocalPeerComm", "LocalPeerCommPostOnly"]
+COMMS = ["LocalComm", "LocalPeerComm", "LocalPeerCommPostOnly", "LocalPeerCommNoFold"]
 
 
 @gpu
@@ -648,8 +648,10 @@ def test_peer_exchange_schedule_is_fresh_and_race_free(monkeypatch, method, extr
             ev.append(("fin",))
             return 0
 
-        def kpl_sweep_peer(self, op, kcfg, vecs, kind, row, ws, pxd, e, par, push, wpar, hs):
+        def kpl_sweep_peer(self, op, kcfg, vecs, kind, row, ws, pxd, e, par, push, wpar, wait_e, wait_par, hs):
             if ws == D0[0]:
+                if wait_e:             # deferred fold: the sweep's CTAs wait (and fold) first
+                    ev.append(("fin",))
                 ev.append(("sweep",) + cur[0])
             pushed = set()
             if push & _lib.KPL_PUSH_W:
@@ -774,3 +776,116 @@ def test_fused_final_record_after_predicated_sweeps():
                             comm=LocalPeerComm(3), zc=1)
     assert res.iterations == ref.iterations and ref.iterations % 10 != 0
     assert [(h.alpha, h.rnorm_true) for h in res.history] == [(h.alpha, h.rnorm_true) for h in ref.history]
+
+
+# ---------------------------------------------------------------- concurrency
+# the ranks' kernels run AT THE SAME TIME (one CUDA stream
+# per virtual rank), so every device flag wait really blocks on a kernel of
+# another rank that is still running.  Grids are small enough to be
+# co-resident on the one GPU (a spinning CTA must not starve the kernel it
+# waits for).  A push that raced a peer's read, a fold of a stale table slot
+# or a missed wait would change bits against the 1-GPU solve; the solve is
+# repeated to give a race many chances.  A short device timeout turns a
+# protocol deadlock into an error instead of a hang.
+
+@pytest.fixture
+def short_peer_timeout():
+    lib = _lib.load()
+    assert lib.kpl_set_peer_timeout(10.0) == 0
+    yield
+    lib.kpl_set_peer_timeout(20.0)
+
+
+def _check_same(res, ref, x):
+    assert res.iterations == ref.iterations and res.converged == ref.converged
+    for a, c in zip(res.history, ref.history):
+        assert (a.alpha, a.beta, a.gamma, a.delta, a.rnorm_recursive, a.rnorm_true) == \
+               (c.alpha, c.beta, c.gamma, c.delta, c.rnorm_recursive, c.rnorm_true)
+    assert x.tobytes() == np.asarray(ref.x).tobytes()
+
+
+@gpu
+@pytest.mark.parametrize("fused,fold", [(True, True), (True, False), (False, False)])
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("method,extra", [("pcg_sh", {"shift": 2.30188679245283}), ("pcg_rr", {}), ("cg", {})])
+def test_concurrent_ranks_slab_bitwise(short_peer_timeout, P, method, extra, fused, fold):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200.distributed import LocalPeerComm, solve_distributed
+    A = K.Stencil3D(128, 64, 32)                       # <= 64 items per rank: co-resident
+    b = K.spmv(A, np.random.default_rng(5).normal(size=A.n))
+    cfg = K.SolverConfig(method=method, max_iters=120, rtol=1e-11, **extra)
+    zc = 4
+    ref = _one_gpu(A, None, b, cfg, zc)
+    plan = SlabPlan(128, 64, 32, P, zc)
+    for rep in range(4):
+        res = solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
+                                comm=LocalPeerComm(P, fused=fused, concurrent=True, fold=fold), zc=zc)
+        torch.cuda.synchronize()
+        _check_same(res, ref, np.concatenate([xi.cpu().numpy() for xi in res.x]))
+
+
+@gpu
+@pytest.mark.parametrize("P", [2, 3])
+def test_concurrent_ranks_rows_bitwise(short_peer_timeout, P):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200 import problems
+    from paper_1706_05988_b200.distributed import LocalPeerComm, solve_distributed
+    A = problems.banded_spd(20000, seed=0, band=2000)
+    M = K.make_jacobi(A)
+    b = K.spmv(A, np.random.default_rng(1).standard_normal(A.n))
+    cfg = K.SolverConfig(method="pcg_sh", shift=0.4124626382901352, max_iters=300, rtol=1e-10)
+    ref = K.solve(A, M, b, None, cfg)
+    plan = RowPlan(A, P)
+    for rep in range(4):
+        res = solve_distributed(A, M, [b[plan.local_slice(r)] for r in range(P)], None, cfg,
+                                comm=LocalPeerComm(P, concurrent=True))
+        torch.cuda.synchronize()
+        _check_same(res, ref, np.concatenate([xi.cpu().numpy() for xi in res.x]))
+
+
+@gpu
+def test_fold_removes_the_finalize_launches(monkeypatch):
+    """With the deferred fold, consecutive fused iteration sweeps have no
+    kpl_peer_finalize between them: only cadence records, polls and the end
+    of the solve still finalize (DESIGN.md 6.1 cost model)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_05988_b200 as K
+    from paper_1706_05988_b200.distributed import LocalPeerComm, solve_distributed
+    A = K.Stencil3D(64, 32, 32)
+    b = K.spmv(A, np.random.default_rng(5).normal(size=A.n))
+    cfg = K.SolverConfig(method="pcg_sh", shift=1.0, max_iters=100, rtol=0.0)
+    plan = SlabPlan(64, 32, 32, 2, 4)
+    counts = {}
+    for fold in (True, False):
+        lib = _lib.load()
+        calls = {"fin": 0, "sweep": 0}
+        real_fin, real_sw = lib.kpl_peer_finalize, lib.kpl_sweep_peer
+
+        class Spy:
+            def __getattr__(self, name):
+                return getattr(lib, name)
+
+            def kpl_peer_finalize(self, *a):
+                calls["fin"] += 1
+                return real_fin(*a)
+
+            def kpl_sweep_peer(self, *a):
+                calls["sweep"] += 1
+                return real_sw(*a)
+
+        spy = Spy()
+        monkeypatch.setattr(_lib, "load", lambda: spy)
+        solve_distributed(A, None, [b[plan.local_slice(r)] for r in range(2)], None, cfg,
+                          comm=LocalPeerComm(2, fold=fold), zc=4)
+        monkeypatch.setattr(_lib, "load", lambda: lib)
+        counts[fold] = dict(calls)
+    assert counts[True]["sweep"] == counts[False]["sweep"]
+    # 100 iterations: without the fold one finalize per fused sweep; with it only
+    # the cadence rows (every 10th) and the host polls keep one
+    assert counts[False]["fin"] >= 2 * 100
+    assert counts[True]["fin"] <= counts[False]["fin"] - 2 * 60

@@ -43,7 +43,8 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
     import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     structs = {"kpl_op": _lib.KplOp, "kpl_cfg": _lib.KplCfg, "kpl_vecs": _lib.KplVecs,
-               "kpl_status": _lib.KplStatus}
+               "kpl_status": _lib.KplStatus, "kpl_copy": _lib.KplCopy, "kpl_post": _lib.KplPost,
+               "kpl_peer_sweep": _lib.KplPeerSweep}
     lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "kpl_b200.h"', "int main(void) {"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
@@ -61,6 +62,34 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
         assert int(got[cname]) == ctypes.sizeof(cls), cname
         for fname, _ in cls._fields_:
             assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, f"{cname}.{fname}"
+
+
+def _integration_stub():
+    """The ctypes stub of INTEGRATION.md section 2, executed as written (its
+    relative `from .solvers import` is satisfied by this package's types)."""
+    import os
+    import re
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    block = re.search(r"```python\n(# kpl/_b200.py.*?)```", text, re.S).group(1)
+    code = block.replace("from .solvers import", "from paper_1706_05988_b200.solvers import")
+    ns = {}
+    exec(compile(code, "INTEGRATION.md:stub", "exec"), ns)
+    return ns
+
+
+def test_integration_stub_structs_match_the_abi():
+    """the stub's structs must have the library's full layout
+    (sizes and every field offset), so a maintainer copying it allocates and
+    fills kpl_op / kpl_cfg / kpl_vecs / kpl_status correctly."""
+    ns = _integration_stub()
+    for stub, mine in ((ns["Op"], _lib.KplOp), (ns["Cfg"], _lib.KplCfg), (ns["Vecs"], _lib.KplVecs),
+                       (ns["Status"], _lib.KplStatus)):
+        assert ctypes.sizeof(stub) == ctypes.sizeof(mine), stub.__name__
+        assert [f for f, _ in stub._fields_] == [f for f, _ in mine._fields_], stub.__name__
+        for f, _ in mine._fields_:
+            assert getattr(stub, f).offset == getattr(mine, f).offset, (stub.__name__, f)
+            assert getattr(stub, f).size == getattr(mine, f).size, (stub.__name__, f)
 
 
 def test_reduction_order_field_validation():

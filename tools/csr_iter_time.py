@@ -1,20 +1,69 @@
-"""Device time of N iteration sweeps (no result check) -- A/B timing helper."""
-import os, sys
+"""Device time of N p-CG-sh iteration sweeps (no result check) -- A/B timing helper.
+
+    KPL_CSR_GATHER=csr|sorted KPL_SORTED_NT=256|512|1024 python tools/csr_iter_time.py [c2c,c4,c5]
+
+Matrices are cached under /tmp/kpl_cache (generation of config 5 takes ~30 s).
+"""
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
-import paper_1706_05988_b200 as K
-from paper_1706_05988_b200 import problems
-from paper_1706_05988_b200.solvers import _Solve
-probs = {
-    "c2c": (K.laplacian_2d(2048, 2048), np.random.default_rng(0).random(2048 * 2048)),
-    "c4": (problems.varcoef_3d(256, seed=0, check_symmetry=False), np.random.default_rng(1).standard_normal(256 ** 3)),
-    "c5": (problems.banded_spd(2_000_000, seed=0), np.random.default_rng(1).standard_normal(2_000_000)),
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1706_05988_b200 as K  # noqa: E402
+from paper_1706_05988_b200 import problems  # noqa: E402
+from paper_1706_05988_b200.solvers import _Solve  # noqa: E402
+
+CACHE = "/tmp/kpl_cache"
+GEN = {
+    "c2c": lambda: K.laplacian_2d(2048, 2048),
+    "c4": lambda: problems.varcoef_3d(256, seed=0, check_symmetry=False),
+    "c5": lambda: problems.banded_spd(2_000_000, seed=0),
 }
-for name, (A, v) in probs.items():
-    M = K.make_jacobi(A)
-    b = torch.as_tensor(v, device="cuda")
-    S = _Solve(A, M, b, None, K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=100))
-    S.init(); S.iterate(1); torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(); S.iterate(9); e1.record(); torch.cuda.synchronize()
-    print(name, os.path.basename(os.environ.get("KPL_LIB", "default")), f"{e0.elapsed_time(e1)/9:.4f} ms/sweep")
+RHS = {
+    "c2c": lambda n: np.random.default_rng(0).random(n),
+    "c4": lambda n: np.random.default_rng(1).standard_normal(n),
+    "c5": lambda n: np.random.default_rng(1).standard_normal(n),
+}
+
+
+def matrix(name):
+    os.makedirs(CACHE, exist_ok=True)
+    f = os.path.join(CACHE, name + ".npz")
+    if os.path.exists(f):
+        d = np.load(f)
+        return K.SparseMatrix(int(d["n"]), d["row_ptr"], d["col_idx"], d["values"], check_symmetry=False)
+    A = GEN[name]()
+    np.savez(f, n=A.n, row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    return A
+
+
+def main():
+    names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c2c", "c4", "c5"]
+    tag = f"gather={os.environ.get('KPL_CSR_GATHER', 'auto')} nt={os.environ.get('KPL_SORTED_NT', '512')}"
+    for name in names:
+        A = matrix(name)
+        M = K.make_jacobi(A)
+        b = torch.as_tensor(RHS[name](A.n), device="cuda")
+        S = _Solve(A, M, b, None, K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=100))
+        S.init()
+        S.iterate(1)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            S.iterate(9)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 9)
+            S = _Solve(A, M, b, None, K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=100))
+            S.init()
+            S.iterate(1)
+            torch.cuda.synchronize()
+        print(name, tag, f"{best:.4f} ms/iteration (best of 3 x 9)", flush=True)
+
+
+if __name__ == "__main__":
+    main()
