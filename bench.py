@@ -213,6 +213,24 @@ def run_ours(args):
     e2e = world * its * args.steps / t_e2e
     hist_bytes = 80 * (its + 1)
 
+    # ---- e2e with the caller's real types: a numpy b in, a numpy x out (pageable
+    # host memory, as a kpl user calls solve), copies inside the timed region
+    b_np = b_host.numpy().copy()
+    K.solve(A, None, b_np, None, cfg)
+    barrier()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    for _ in range(args.steps):
+        r3 = K.solve(A, None, b_np, None, cfg)
+        assert isinstance(r3.x, np.ndarray)
+        its_np = r3.iterations
+        del r3
+    g1.record()
+    barrier()
+    t_np = max_over_ranks(g0.elapsed_time(g1) / 1000.0)
+    e2e_np = world * its_np * args.steps / t_np
+    del b_np
+
     # ---- dominant kernel: the fused p-CG-sh iteration sweep, timed alone
     S = _Solve(A, None, b, None, K.SolverConfig(method="pcg_sh", shift=SIGMA, max_iters=100, rtol=0.0))
     S.init()
@@ -258,7 +276,11 @@ def run_ours(args):
         "hbm_gbs": hbm_gbs,
         "hbm_frac_of_measured": hbm_gbs / peak / world,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-                "d2h_bytes_per_step": 8 * n + hist_bytes + 128},
+                "d2h_bytes_per_step": 8 * n + hist_bytes + 128,
+                "host_buffers": "pinned torch CPU tensors (b in, x out)"},
+        "e2e_numpy": {"value": e2e_np, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                      "d2h_bytes_per_step": 8 * n + hist_bytes + 128,
+                      "host_buffers": "numpy arrays (pageable): the kpl caller's own types"},
         "roofline": {
             "bound": "hbm",
             "achieved": achieved,
@@ -298,6 +320,7 @@ def run_distributed(args, rank, world, local):
     plan = SlabPlan(N3, N3, N3, world)
     b_full = K.spmv(A, torch.full((n,), 1.0 / math.sqrt(n), dtype=torch.float64, device=dev))
     b = b_full[plan.local_slice(rank)].clone()
+    bnorm = float(torch.linalg.norm(b_full))
     del b_full
     torch.cuda.empty_cache()
     # device-initiated exchange over NVLink peer memory (kpl_peer_post /
@@ -307,12 +330,24 @@ def run_distributed(args, rank, world, local):
     # wait on one another.
     exchange = os.environ.get("KPL_DIST_EXCHANGE", "peer" if dist.get_backend() == "nccl" else "host")
     comm = None
+    check = None
     if exchange == "peer":
         why = ""
         try:
+            # self-check before trusting the device-initiated exchange: 12
+            # iterations (cadence rows, deferred folds, halo pushes) through PeerComm must
+            # equal the host-driven NCCL exchange bit for bit on every rank
             comm = PeerComm()
-            solve_distributed(A, None, b, None, K.SolverConfig(method="pcg_sh", shift=SIGMA, max_iters=2,
-                                                               rtol=0.0), comm=comm)
+            pcfg = K.SolverConfig(method="pcg_sh", shift=SIGMA, max_iters=12, rtol=0.0)
+            rp = solve_distributed(A, None, b, None, pcfg, comm=comm)
+            rh = solve_distributed(A, None, b, None, pcfg, comm=TorchComm())
+            same = (rp.iterations == rh.iterations and all(
+                (a.alpha, a.beta, a.gamma, a.delta, a.rnorm_recursive, a.rnorm_true) ==
+                (c.alpha, c.beta, c.gamma, c.delta, c.rnorm_recursive, c.rnorm_true)
+                for a, c in zip(rp.history, rh.history)) and bool(torch.equal(rp.x[0], rh.x[0])))
+            check = "peer == host exchange, bitwise (12 iterations)" if same else "MISMATCH"
+            if not same:
+                why = f"rank {rank}: peer exchange result differs from the host-driven exchange"
         except Exception as exc:          # IPC unavailable: use the host-driven path (all ranks)
             why = f"rank {rank}: {exc}"
         verdicts = [None] * world
@@ -375,6 +410,8 @@ def run_distributed(args, rank, world, local):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated operator and rhs; no dataset)",
         "config": {"workload": WORKLOAD, "n": n, "iterations_per_step": res.iterations,
+                   "final_true_rel_residual": res.history[-1].rnorm_true / bnorm,
+                   "exchange_check": check,
                    "parallelism": (f"z-slab x{world} (NVLink peer-memory halos + partials, device flags)"
                                    if exchange == "peer" else
                                    f"z-slab x{world} ({dist.get_backend()} halo send/recv + chunk all-gather)"),
@@ -426,6 +463,26 @@ def cpu_iterations(nsteps, O=None, A=None, b=None, warm=0):
     return times
 
 
+def host_cpu():
+    """CPU model and core count of the host the baseline ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cores": os.cpu_count()}
+
+
+PORT_NOTE = ("the oracle port is matrix-free (the reference assembles a 512^3 int64 CSR, ~50-60 GB); "
+             "at 128^3 the reference ran 1.8x slower per DOF than this port (BASELINE.md 2), so the port "
+             "overstates the reference's speed; the reference itself is timed on configs 1, 2 and 5 in "
+             "profiles/r02_reference_cpu.jsonl (tools/time_reference.py)")
+
+
 def cpu_baseline(iters):
     O, A, b = _cpu_setup()
     times = cpu_iterations(iters, O, A, b, warm=0)
@@ -434,7 +491,7 @@ def cpu_baseline(iters):
             "sample": (f"{len(times)} p-CG-sh iterations of the 512^3 problem with the CPU "
                        "oracle (numpy ufuncs + C restatement of the reference's kernels, "
                        "single thread like the reference); includes its true-residual cadence"),
-            "seconds_per_iteration": per}
+            "seconds_per_iteration": per, **host_cpu(), "note": PORT_NOTE}
 
 
 def run_reference(args):
@@ -456,7 +513,7 @@ def run_reference(args):
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": f"{steps} iterations of the 512^3 problem, oracle restatement "
-                                   "of the single-threaded reference path"},
+                                   "of the single-threaded reference path", **host_cpu(), "note": PORT_NOTE},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)

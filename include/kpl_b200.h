@@ -208,6 +208,21 @@ int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
    multiple of 10.                                                          */
 int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
                        int64_t first, int64_t count, void *workspace, void *stream);
+/* kpl_solver_iterate with flags.  KPL_ITER_LAZY_REPLACE (p-CG-rr): do not
+   enqueue the four residual-replacement sweeps (solvers.py:599-607) after
+   every iteration; when the device trigger fires, the following iterations
+   are predicated off (the status shows fire = 1 at row iter) until the host
+   calls kpl_solver_replace and re-issues from index iter + 1.  The executed
+   operations -- and so every bit of the result -- are the same as with the
+   eager sequence; the idle replacement launches disappear.               */
+#define KPL_ITER_LAZY_REPLACE 1
+int kpl_solver_iterate2(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v,
+                        int64_t first, int64_t count, int32_t flags, void *workspace, void *stream);
+/* Enqueue the residual replacement r = b - A x, u = M r, w = A u, s = A p,
+   q = M s, z = A q + the record of the replaced row (solvers.py:600-607),
+   predicated on the device trigger.                                       */
+int kpl_solver_replace(const kpl_op *op, const kpl_cfg *cfg, const kpl_vecs *v, void *workspace,
+                       void *stream);
 /* Same as kpl_solver_iterate, as ONE cooperative (persistent) launch with a
    grid barrier between passes -- for small problems where per-iteration
    launch latency dominates.  Single-GPU stencil p-CG / p-CG-sh / p-CG-var-sh

@@ -74,6 +74,7 @@ class KplPost(ctypes.Structure):
 
 
 KPL_PUSH_W, KPL_PUSH_X = 1, 2
+KPL_ITER_LAZY_REPLACE = 1
 
 
 class KplPeerSweep(ctypes.Structure):
@@ -99,6 +100,10 @@ _SIGS = {
                                ctypes.POINTER(KplVecs), _p, _p, _p]),
     "kpl_solver_iterate": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
                                   ctypes.POINTER(KplVecs), _i64, _i64, _p, _p]),
+    "kpl_solver_iterate2": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
+                                   ctypes.POINTER(KplVecs), _i64, _i64, _i32, _p, _p]),
+    "kpl_solver_replace": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
+                                  ctypes.POINTER(KplVecs), _p, _p]),
     "kpl_solver_iterate_persistent": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),
                                              ctypes.POINTER(KplVecs), _i64, _i64, _p, _p]),
     "kpl_solver_cg_pass": (_i32, [ctypes.POINTER(KplOp), ctypes.POINTER(KplCfg),

@@ -21,6 +21,7 @@
 #include "kpl_tma.cuh"
 #include "kpl_ic0.cuh"
 #include "kpl_peer.cuh"
+#include "kpl_spmv_tma.cuh"
 
 using namespace kpl;
 
@@ -255,6 +256,18 @@ void launch_sorted(const kpl_op *op, const CGeo &g, const SIn &in, double *out, 
     const SGather sg{op->sp_col, op->sp_val, reinterpret_cast<const unsigned short *>(op->sp_dest), op->sp_rows};
     const long long nblk = cdiv(op->n, op->sp_rows);
     // idle replacement sweeps (PRED_FIRE) keep a small grid, as the other sweeps
+    // default: the bulk-TMA-fed kernel (matrix stream off the LSU queue), one CTA per SM
+    static const bool plain = [] { const char *e = std::getenv("KPL_SORTED_KERNEL"); return e && !std::strcmp(e, "plain"); }();
+    using RG = SpRing<2048, 2>;
+    const size_t tsmem = RG::bytes(op->sp_max);
+    static const int lag = [] { const char *e = std::getenv("KPL_SORTED_LAG"); return e ? std::atoi(e) : 2; }();
+    if (!plain && tsmem <= 227 * 1024) {
+        auto kern = lag == 1 ? csr_sorted_tma_spmv<SIn, 512, 2048, 2, 1> : csr_sorted_tma_spmv<SIn, 512, 2048, 2, 2>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+        const unsigned tgrid = (unsigned)std::min(nblk, (long long)kSMs);
+        launch_pdl(kern, tgrid, 512 + 32, tsmem, st, g, sg, in, out, ws, pred, row);
+        return;
+    }
     const size_t smem = 8 * (size_t)op->sp_max;
     // persistent: one CTA per SM (two when the products fit twice), striding over the
     // blocks so the next block's first stream loads overlap this block's row sums
@@ -267,6 +280,23 @@ void launch_sorted(const kpl_op *op, const CGeo &g, const SIn &in, double *out, 
         if (per == 8) launch_sorted_nt<SIn, 512, 8>(g, sg, in, out, ws, pred, row, grid, smem, st);
         else launch_sorted_nt<SIn, 512, 4>(g, sg, in, out, ws, pred, row, grid, smem, st);
     }
+}
+
+// CSR-order SpMV: KPL_SPMV=plain keeps the one-window-at-a-time kernel for A/B
+// runs; the default pipelines the next window's loads under the row sums.
+template <class SIn>
+void launch_csr_spmv(bool long_rows, unsigned grid, cudaStream_t st, const CGeo &g, const SIn &in, double *out,
+                     const Ws &ws, int pred, long long row) {
+    static const bool plain = [] { const char *e = std::getenv("KPL_SPMV"); return e && !std::strcmp(e, "plain"); }();
+    if (plain) {
+        if (long_rows) launch_pdl(csr_spmv_kernel<SIn, 512>, grid, NT, 0, st, g, in, out, ws, pred, row);
+        else launch_pdl(csr_spmv_kernel<SIn, CSR_WIN, true>, grid, NT, 0, st, g, in, out, ws, pred, row);
+        return;
+    }
+    // long scattered rows: the pipelined kernel (config 5: 0.301 -> 0.287 ms/iteration); short rows keep
+    // the one-window kernel at 8 CTAs/SM (pipelined at 6 CTAs/SM: config 4 0.786 -> 0.825, 2-CSR 0.200 -> 0.211)
+    if (long_rows) launch_pdl(csr_spmv_pipe<SIn, 512, false, 8>, grid, NT, 0, st, g, in, out, ws, pred, row);
+    else launch_pdl(csr_spmv_kernel<SIn, CSR_WIN, true>, grid, NT, 0, st, g, in, out, ws, pred, row);
 }
 
 // `spin`: input of the CSR SpMV when it differs from the body's stencil input
@@ -302,14 +332,9 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
                 if constexpr (std::is_same<SpIn, NoSpmvIn>::value) launch_sorted(op, g, in, ws.nbuf, ws, pred, row, st);
                 else launch_sorted(op, g, spin, ws.nbuf, ws, pred, row, st);
             } else if constexpr (std::is_same<SpIn, NoSpmvIn>::value) {
-                if (long_rows) launch_pdl(csr_spmv_kernel<In, 512>, sgrid, NT, 0, st, g, in, ws.nbuf, ws, pred, row);
-                else launch_pdl(csr_spmv_kernel<In, CSR_WIN, true>, sgrid, NT, 0, st, g, in, ws.nbuf, ws, pred, row);
+                launch_csr_spmv(long_rows, sgrid, st, g, in, ws.nbuf, ws, pred, row);
             } else {
-                if (long_rows)
-                    launch_pdl(csr_spmv_kernel<SpIn, 512>, sgrid, NT, 0, st, g, spin, ws.nbuf, ws, pred, row);
-                else
-                    launch_pdl(csr_spmv_kernel<SpIn, CSR_WIN, true>, sgrid, NT, 0, st, g, spin, ws.nbuf, ws, pred,
-                               row);
+                launch_csr_spmv(long_rows, sgrid, st, g, spin, ws.nbuf, ws, pred, row);
             }
         }
         launch_pdl(csr_chunk_sweep<In, Body, true>, (unsigned)std::min(L.nch, cap), NT, 0, st, g, L, in, body,
@@ -676,7 +701,9 @@ int kind_phase(int kind, int &phase, int &pred) {
     case KPL_SW_BNORM: phase = PH_BNORM; pred = PRED_ALWAYS; return KPL_OK;
     case KPL_SW_INIT_R: phase = PH_INITR; pred = PRED_ALWAYS; return KPL_OK;
     case KPL_SW_INIT_W: phase = PH_PIPE; pred = PRED_ALWAYS; return KPL_OK;
-    case KPL_SW_ITER: phase = PH_PIPE; pred = PRED_RUNNING; return KPL_OK;
+    // an iteration never runs over a pending residual replacement (p-CG-rr with the
+    // replacement issued by the host on demand: kpl_solver_iterate2 + kpl_solver_replace)
+    case KPL_SW_ITER: phase = PH_PIPE; pred = PRED_NOFIRE; return KPL_OK;
     case KPL_SW_TRUE: phase = PH_TRUE; pred = PRED_ROW; return KPL_OK;
     case KPL_SW_CG_P: phase = PH_CGDELTA; pred = PRED_RUNNING; return KPL_OK;
     case KPL_SW_CG_X: phase = PH_CGHEAD; pred = PRED_RUNNING; return KPL_OK;
@@ -988,10 +1015,27 @@ int kpl_solver_init(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, co
 
 int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t first,
                        int64_t count, void *workspace, void *stream) {
+    return kpl_solver_iterate2(op, cfgp, v, first, count, 0, workspace, stream);
+}
+
+int kpl_solver_replace(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, void *workspace, void *stream) {
+    Ctx c;
+    int rc = make_ctx(op, cfgp, v, workspace, stream, c);
+    if (rc != KPL_OK) return rc;
+    if (c.cfg.method != KPL_M_PCG_RR) return fail(KPL_EINVAL, "replacement is a p-CG-rr step");
+    for (int k : {KPL_SW_RR_R, KPL_SW_RR_W, KPL_SW_RR_S, KPL_SW_RR_Z})
+        if ((rc = do_sweep(c, k, 0)) != KPL_OK) return rc;
+    return KPL_OK;
+}
+
+int kpl_solver_iterate2(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v, int64_t first,
+                        int64_t count, int32_t flags, void *workspace, void *stream) {
     Ctx c;
     int rc = make_ctx(op, cfgp, v, workspace, stream, c);
     if (rc != KPL_OK) return rc;
     if (op->chunks_global > 0) return fail(KPL_EINVAL, "multi-GPU operators are driven sweep by sweep");
+    if (flags & ~KPL_ITER_LAZY_REPLACE) return fail(KPL_EINVAL, "unknown iterate flags");
+    const bool lazy = (flags & KPL_ITER_LAZY_REPLACE) != 0;
     for (int64_t j = first; j < first + count; ++j) {
         if ((rc = record_sweeps(c, j, true)) != KPL_OK) return rc;
         if (c.cfg.method == KPL_M_CG) {
@@ -1000,7 +1044,7 @@ int kpl_solver_iterate(const kpl_op *op, const kpl_cfg *cfgp, const kpl_vecs *v,
             continue;
         }
         if ((rc = do_sweep(c, KPL_SW_ITER, 0)) != KPL_OK) return rc;
-        if (c.cfg.method == KPL_M_PCG_RR) {
+        if (c.cfg.method == KPL_M_PCG_RR && !lazy) {
             // explicit replacement, predicated on the device trigger (solvers.py:599-607)
             for (int k : {KPL_SW_RR_R, KPL_SW_RR_W, KPL_SW_RR_S, KPL_SW_RR_Z})
                 if ((rc = do_sweep(c, k, 0)) != KPL_OK) return rc;

@@ -59,6 +59,7 @@ enum Pred : int {
     PRED_RUNNING = 1,        // state == RUNNING
     PRED_FIRE = 2,           // state == RUNNING && fire  (pcg_rr replacement)
     PRED_ROW = 3,            // head.iter == row (explicit true-residual row)
+    PRED_NOFIRE = 4,         // state == RUNNING && !fire  (an iteration waits for a pending replacement)
 };
 
 struct Layout {               // identical on host and device
@@ -437,6 +438,7 @@ __device__ __forceinline__ bool pred_ok(const WsHead *h, int pred, long long row
     case PRED_RUNNING: return state == KPL_ST_RUNNING;
     case PRED_FIRE: return state == KPL_ST_RUNNING && ld_head(&h->fire) != 0;
     case PRED_ROW: return ld_head(&h->iter) == row && state != KPL_ST_BREAKDOWN;
+    case PRED_NOFIRE: return state == KPL_ST_RUNNING && ld_head(&h->fire) == 0;
     default: return true;
     }
 }

@@ -509,6 +509,67 @@ csr_spmv_kernel(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long l
     }
 }
 
+// Software-pipelined form of csr_spmv_kernel: the products of window k go to
+// one of two shared-memory buffers, then window k+1's col/val loads and
+// gathers are issued BEFORE the barrier and the row sums of window k, so they
+// are in flight while the CTA sums (one __syncthreads per window instead of
+// two).  Same products, same csr_matvec order: bitwise equal.
+template <class In, int WIN, bool L2G, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+csr_spmv_pipe(CGeo g, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
+    constexpr int PER = WIN / NT;
+    __shared__ double sprod[2][WIN];
+    pdl_wait();
+    pdl_launch_dependents();
+    if (ws.head && !pred_ok(ws.head, pred, row)) return;
+    if (ws.head) in.setup(ws);
+    const int tid = threadIdx.x;
+    const long long nblk = (g.n + RB - 1) / RB;
+    const double *base = in.base();
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const long long r0 = blk * RB;
+        const long long r = r0 + tid;
+        const bool ok = r < g.n;
+        const long long rend = min(r0 + RB, g.n);
+        const long long k0 = __ldg(g.row_ptr + r0), k1 = __ldg(g.row_ptr + rend);
+        long long lo = 0, hi = 0;
+        if (ok) { lo = __ldg(g.row_ptr + r); hi = __ldg(g.row_ptr + r + 1); }
+        int col[PER];
+        double val[PER], raw[PER];
+        auto issue = [&](long long wk) {          // col/val of window wk, then its gathers
+            const long long we = min(wk + (long long)WIN, k1);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const long long kk = wk + tid + (long long)j * NT;
+                col[j] = 0; val[j] = 0.0;
+                if (kk < we) { col[j] = __ldcs(g.col_idx + kk); val[j] = __ldcs(g.values + kk); }
+            }
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const long long kk = wk + tid + (long long)j * NT;
+                raw[j] = kk < we ? load1<L2G>(in, base, col[j]) : 0.0;
+            }
+        };
+        double a = 0.0;
+        if (k0 < k1) issue(k0);
+        int buf = 0;
+        for (long long wk = k0; wk < k1; wk += WIN, buf ^= 1) {
+            const long long we = min(wk + (long long)WIN, k1);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const long long kk = wk + tid + (long long)j * NT;
+                if (kk < we) sprod[buf][kk - wk] = __dmul_rn(val[j], in.xf(raw[j], col[j]));
+            }
+            if (we < k1) issue(we);                  // next window in flight during the sums
+            __syncthreads();
+            const long long a0 = max(lo, wk), a1 = min(hi, we);
+            for (long long kk = a0; kk < a1; ++kk) a = __dadd_rn(a, sprod[buf][kk - wk]);   // csr_matvec order
+        }
+        if (ok) out[r] = a;
+        __syncthreads();          // the next block reuses both buffers
+    }
+}
+
 // Column-sorted gather form of csr_spmv_kernel (kpl_op.sp_*; scattered
 // matrices such as config 5's random band, where a CSR-order warp gather
 // touches ~31 cache lines and the SpMV is bound by L1 wavefronts).  One CTA

@@ -118,12 +118,16 @@ class DeviceMatrix:
             self.sorted = sorted_gather_layout(A.row_ptr, A.col_idx, self.row_ptr, self.col_idx, self.values)
 
 
-# Column-sorted SpMV gathers (kpl_op.sp_*): worth it when a CSR-order warp
-# gather touches many cache lines (config 5's random band: ~31 of 32 lanes on
-# distinct 128-byte lines; a 7-point stencil matrix: ~6).  KPL_CSR_GATHER =
-# auto (default) | csr | sorted.
+# Column-sorted SpMV gathers (kpl_op.sp_*): meant for matrices whose CSR-order
+# warp gathers touch many cache lines (config 5's random band: ~31 of 32 lanes
+# on distinct 128-byte lines; a 7-point stencil matrix: ~6).  Measured on
+# config 5 it only matches the pipelined CSR-order kernel (0.304 vs 0.287
+# ms/iteration), so it is opt-in: KPL_CSR_GATHER = csr (default)
+# | sorted | auto (sorted when a CSR-order warp gather touches >= 12 lines).
 _SORTED_MIN_LINES = 12.0
-_SORTED_MAX_NNZ = 27 * 1024            # products per block in shared memory (216 KiB)
+# products of one block live in shared memory next to the bulk-copy ring of
+# csr_sorted_tma_spmv (2 x 2048 nonzeros x 14 B): 227 KiB - 56 KiB -> 21,872
+_SORTED_MAX_NNZ = 21_800
 
 
 def csr_lines_per_warp(col_idx, sample=1 << 16):
@@ -141,7 +145,7 @@ def sorted_gather_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values):
     """(sp_col, sp_val, sp_dest, rows per block, max block nnz) or None.  Index
     work only (the values are permuted, never combined), done once per matrix
     with device sorts."""
-    mode = os.environ.get("KPL_CSR_GATHER", "auto")
+    mode = os.environ.get("KPL_CSR_GATHER", "csr")
     if mode not in ("auto", "csr", "sorted"):
         raise ValueError(f"KPL_CSR_GATHER={mode!r}: expected auto, csr or sorted")
     if mode == "csr" or (mode == "auto" and csr_lines_per_warp(col_idx_h) < _SORTED_MIN_LINES):
@@ -149,7 +153,7 @@ def sorted_gather_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values):
     rp = np.asarray(row_ptr_h, dtype=np.int64)
     n = len(rp) - 1
     R = 0
-    for cand in (1024, 512, 256, 128, 64, 32):
+    for cand in list(range(1024, 0, -64)) + [32, 16, 8]:     # the largest block that fits
         ends = np.minimum(np.arange(0, n, cand) + cand, n)
         most = int((rp[ends] - rp[np.arange(0, n, cand)]).max()) if n else 0
         if most <= _SORTED_MAX_NNZ:
@@ -162,11 +166,14 @@ def sorted_gather_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values):
     blk = t.repeat_interleave(t.arange(n, device=row_ptr.device) // R, counts)
     perm = t.argsort(blk * (1 << 31) + col_idx.long())
     del counts
-    sp_col = col_idx[perm].contiguous()
-    sp_val = values[perm].contiguous()
+    nnz = int(col_idx.numel())
+    pad = lambda a: t.cat([a, a.new_zeros(8)])      # 8 entries: the last 16-byte bulk copy may over-read
+    sp_col = pad(col_idx[perm])
+    sp_val = pad(values[perm])
     first = row_ptr.long()[blk[perm] * R]
-    sp_dest = (perm - first).to(t.int32).to(t.int16).contiguous()     # < 65536: uint16 bits
+    sp_dest = pad((perm - first).to(t.int32).to(t.int16))             # < 65536: uint16 bits
     del blk, perm, first
+    assert sp_col.numel() == nnz + 8
     return sp_col, sp_val, sp_dest, R, most
 
 

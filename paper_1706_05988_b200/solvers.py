@@ -237,6 +237,11 @@ class _Solve:
                           and cfg.method in ("pcg", "pcg_sh", "pcg_var_sh") and not cfg.track_gaps
                           and self.op.order == _lib.KPL_ORDER_TREE)
         self.persistent = bool(persistent)
+        # p-CG-rr: replacement sweeps only when the device trigger fired (host-issued
+        # at the next status poll) instead of four predicated launches per iteration;
+        # KPL_RR_EAGER=1 keeps the per-iteration launches
+        self.lazy_rr = (cfg.method == "pcg_rr" and not self.persistent
+                        and os.environ.get("KPL_RR_EAGER") != "1")
         # classic CG records row i in the first half of pass i, so the final
         # row max_iters needs one more pass than the pipelined solvers
         self.limit = cfg.max_iters + (1 if cfg.method == "cg" else 0)
@@ -253,10 +258,25 @@ class _Solve:
         count = min(count, self.limit - self.issued)
         if count <= 0:
             return
-        fn = lib.kpl_solver_iterate_persistent if self.persistent else lib.kpl_solver_iterate
-        _lib.check(fn(self.op, self.kcfg, self.vecs, self.issued, count, D.ptr(self.ws),
-                      D.stream_handle()), "solver iterate")
+        if self.persistent:
+            _lib.check(lib.kpl_solver_iterate_persistent(self.op, self.kcfg, self.vecs, self.issued, count,
+                                                         D.ptr(self.ws), D.stream_handle()), "solver iterate")
+        else:
+            flags = _lib.KPL_ITER_LAZY_REPLACE if self.lazy_rr else 0
+            _lib.check(lib.kpl_solver_iterate2(self.op, self.kcfg, self.vecs, self.issued, count, flags,
+                                               D.ptr(self.ws), D.stream_handle()), "solver iterate")
         self.issued += count
+
+    def replace_if_fired(self, st):
+        """Lazy p-CG-rr: the trigger fired at record row st.iter + 1 and the
+        iterations issued after it were predicated off -- run the replacement
+        (which records that row) and continue from there."""
+        if not (self.lazy_rr and st.state == _lib.KPL_ST_RUNNING and st.fire):
+            return False
+        _lib.check(_lib.load().kpl_solver_replace(self.op, self.kcfg, self.vecs, D.ptr(self.ws),
+                                                  D.stream_handle()), "replacement")
+        self.issued = int(st.iter) + 1
+        return True
 
     def read_status(self):
         _lib.check(_lib.load().kpl_read_status(D.ptr(self.ws), self.status, D.stream_handle()),
@@ -295,14 +315,20 @@ class _Solve:
         st = self.read_status()
         if callback is not None:
             self._callback(callback)
-        while st.state == _lib.KPL_ST_RUNNING and self.issued < self.limit:
+        while st.state == _lib.KPL_ST_RUNNING and (self.issued < self.limit or st.fire):
+            if self.replace_if_fired(st):
+                st = self.read_status()
+                if callback is not None and st.state != _lib.KPL_ST_BREAKDOWN:
+                    self._callback(callback)
+                continue
             self.iterate(chunk)
             st = self.read_status()
             if callback is not None:
-                if st.state != _lib.KPL_ST_BREAKDOWN:
+                if st.state != _lib.KPL_ST_BREAKDOWN and not st.fire:
                     self._callback(callback)
             else:
-                chunk = min(chunk * 2, 256)
+                # lazy p-CG-rr: a fired trigger idles the rest of the chunk, so keep chunks short
+                chunk = min(chunk * 2, 32 if self.lazy_rr else 256)
         return self.result()
 
     # -- results ---------------------------------------------------------

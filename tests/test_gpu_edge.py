@@ -98,3 +98,32 @@ def test_dispatch_matches_direct_call(method, extra):
     assert _rows(a) == _rows(c)
     assert np.asarray(a.x).tobytes() == np.asarray(c.x).tobytes()
     assert a.replacements == c.replacements
+
+
+@gpu
+@pytest.mark.parametrize("form", ["stencil", "csr"])
+@pytest.mark.parametrize("with_callback", [False, True])
+def test_lazy_replacement_equals_eager(monkeypatch, form, with_callback):
+    """p-CG-rr issues its replacement sweeps only when the device trigger fired
+    (kpl_solver_iterate2 KPL_ITER_LAZY_REPLACE + kpl_solver_replace) instead of
+    four predicated launches per iteration; every bit must be the same as the
+    eager sequence (KPL_RR_EAGER=1), replacement list and callbacks included."""
+    _need_gpu()
+    A = K.Stencil2D(200, 200) if form == "stencil" else K.laplacian_2d(200, 200)
+    b = np.full(A.n, 1 / np.sqrt(A.n))
+    cfg = K.SolverConfig(method="pcg_rr", max_iters=500, rtol=0.0)
+    out = {}
+    for eager in ("1", "0"):
+        monkeypatch.setenv("KPL_RR_EAGER", eager)
+        seen = []
+        cb = (lambda st: seen.append((st.iter, float(np.asarray(st.r)[7])))) if with_callback else None
+        res = K.solve(A, None, b, None, cfg, callback=cb)
+        out[eager] = (res, seen)
+    (e, se), (l, sl) = out["1"], out["0"]
+    assert len(e.replacements) >= 10 and e.replacements == l.replacements
+    assert e.iterations == l.iterations
+    for a, c in zip(e.history, l.history):
+        assert (a.alpha, a.beta, a.gamma, a.delta, a.rnorm_recursive, a.rnorm_true) == \
+               (c.alpha, c.beta, c.gamma, c.delta, c.rnorm_recursive, c.rnorm_true)
+    assert np.asarray(e.x).tobytes() == np.asarray(l.x).tobytes()
+    assert se == sl

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Set up one BASELINE config and run a few solver iterations (ncu target).
 
-    python tools/profile_target.py c4|c5|c2s|c2c|c3 [iters]
+    python tools/profile_target.py c4|c5|c2s|c2c|c3 [iters] [method]
 """
 import math
 import os
@@ -18,6 +18,7 @@ from paper_1706_05988_b200 import problems  # noqa: E402
 def main():
     which = sys.argv[1]
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    method = sys.argv[3] if len(sys.argv) > 3 else "pcg_sh"
     dev = "cuda"
     if which == "c4":
         A = problems.varcoef_3d(256, seed=0, check_symmetry=False)
@@ -39,7 +40,7 @@ def main():
         M = None
         b = K.spmv(A, torch.full((A.n,), 1 / math.sqrt(A.n), dtype=torch.float64, device=dev))
         sig = 2.30188679245283
-    cfg = K.SolverConfig(method="pcg_sh", shift=sig, max_iters=iters, rtol=0.0)
+    cfg = K.SolverConfig(method=method, shift=sig if method == "pcg_sh" else 0.0, max_iters=iters, rtol=0.0)
     res = K.solve(A, M, b, None, cfg)
     torch.cuda.synchronize()
     print(which, A.n, res.iterations, res.history[-1].rnorm_true)
