@@ -184,7 +184,7 @@ class _Solve:
     PERSISTENT_MAX_N_2D = 1 << 18
 
     def __init__(self, A, M, b, x0, cfg: SolverConfig, *, zc=0, vx=0, chunk_blocks=0, slab_view=False,
-                 persistent=None):
+                 persistent=None, alloc=None):
         self.device = dev = D.require_cuda()
         t = D.torch()
         self.cfg = cfg
@@ -203,7 +203,10 @@ class _Solve:
         self.kcfg, self._keep = make_kcfg(cfg, A, self.dm, dev)
         ident = self.dp.identity
         f64 = dict(dtype=t.float64, device=dev)
-        emp = lambda: t.empty(n, **f64)
+        # `alloc(count, dtype)`: where the solver's vectors and workspace live (default: the
+        # torch caching allocator; the guard-band tests pass views into poisoned arenas)
+        alloc = alloc or (lambda cnt, dt: t.empty(cnt, dtype=dt, device=dev))
+        emp = lambda: alloc(n, t.float64)
         self.x = emp()
         self.r = emp()
         self.u = self.r if ident else emp()
@@ -225,7 +228,7 @@ class _Solve:
         lib = _lib.load()
         nbytes = lib.kpl_workspace_bytes(self.op, cfg.max_iters)
         _lib.check(nbytes if nbytes < 0 else 0, "workspace size")
-        self.ws = t.empty(int(nbytes), dtype=t.uint8, device=dev)
+        self.ws = alloc(int(nbytes), t.uint8)
         self.hist_off = lib.kpl_history_offset(self.op)
         self.reps_off = lib.kpl_replacements_offset(self.op, cfg.max_iters)
         self.status = _lib.KplStatus()

@@ -37,6 +37,12 @@ REF = {  # (iterations, final true relative residual)
     ("2", "pcg_sh"): (4764, 9.949e-11),
     ("5", "cg"): (88, 5.746e-11), ("5", "pcg"): (88, 5.758e-11),
     ("5", "pcg_sh"): (88, 5.746e-11), ("5", "pcg_rr"): (88, 5.746e-11),
+    # config 4 (256^3): the full-size oracle in the reference order (tests/golden/config4_oracle_*.npz,
+    # tools/oracle_fullsize.py); the sigma* = 0.49238826317067413 of the rule at 256^3
+    # (profiles/r02_sigma_config4.jsonl) -- every sigma > 0 of the sweep is held to CG's target
+    ("4", "cg"): (2960, 1.0581659160347994e-12),
+    ("4", "pcg_sh x0.25"): (2960, 1.0581659160347994e-12), ("4", "pcg_sh x0.5"): (2960, 1.0581659160347994e-12),
+    ("4", "pcg_sh x1.0"): (2960, 1.0581659160347994e-12),
 }
 
 
@@ -104,10 +110,13 @@ def config4():
     b = dev(np.random.default_rng(1).standard_normal(A.n))
     bn = math.sqrt(K.dot(b, b, A))
     per = 152 * A.n + 12 * A.nnz + 4 * (A.n + 1)
-    sig_star = 0.49238826317067413   # Jacobi-grid rule value at 16^3 / 64^3
+    sig_star = 0.49238826317067413   # the rule at 256^3 (tools/sigma_config4.py, profiles/r02_sigma_config4.jsonl)
     for f in (0.25, 0.5, 1.0):
         cfg = K.SolverConfig(method="pcg_sh", shift=f * sig_star, max_iters=20000, rtol=1e-12)
         report("4", "csr", f"pcg_sh x{f}", cfg.shift, A, M, b, cfg, per, bn)
+    # sigma = 0 (plain p-CG): stagnates above 1e-12, so capped; the run is also the rule's history
+    cfg = K.SolverConfig(method="pcg", max_iters=60000, rtol=1e-12)
+    report("4", "csr", "pcg_sh x0 (= pcg, capped 60000)", 0.0, A, M, b, cfg, per, bn)
     cfg = K.SolverConfig(method="cg", max_iters=20000, rtol=1e-12)
     report("4", "csr", "cg", 0.0, A, M, b, cfg, per, bn)
 

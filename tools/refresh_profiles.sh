@@ -8,4 +8,4 @@ timeout 900 python tools/bench_configs.py > gpurun_out/configs.jsonl 2> gpurun_o
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "launches rc=$?"
 timeout 600 ncu --set full --import-source on --clock-control none -k tma_sweep -s 6 -c 1 \
-    -o gpurun_out/prof_iter python tools/stencil_iter_time.py > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+    -o gpurun_out/prof_iter python tools/stencil_iter_time.py --grid 3d512 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
