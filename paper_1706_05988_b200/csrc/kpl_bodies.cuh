@@ -390,6 +390,10 @@ struct BodyPcgIter {
     }
 };
 
+// bodies a deferred peer fold may precede (kpl_sweep_peer, KPL_SW_ITER)
+template <class B> struct is_pcg_iter : std::false_type {};
+template <int PC, bool VAR> struct is_pcg_iter<BodyPcgIter<PC, VAR>> : std::true_type {};
+
 // track_gaps record sweeps (solvers.py:142-167, gap_vectors / measure_gaps):
 //   F: input x;  t = b - A x -> (t,t), (t - r, t - r)
 //   G: input p;  axpy(-sigma_prev, t, A p) - s

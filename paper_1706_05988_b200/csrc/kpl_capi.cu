@@ -312,6 +312,20 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
     if (op->kind == KPL_OP_STENCIL) {
         SGeo g{op->nx, op->ny, op->nz, op->diag, op->halo_lo, op->halo_hi, op->zhalo};
         const unsigned grid = (unsigned)std::min(L.items, cap);
+        const bool fold = ws.px && ws.wait_epoch;          // deferred peer fold (kpl_sweep_peer)
+        if constexpr (is_pcg_iter<Body>::value) {
+            if (fold) {
+                if (L.vx == 2)
+                    launch_pdl(stencil_sweep<2, In, Body, true>, grid, NT, 0, st, g, L, in, body, ws, cfg, phase,
+                               pred, row);
+                else
+                    launch_pdl(stencil_sweep<1, In, Body, true>, grid, NT, 0, st, g, L, in, body, ws, cfg, phase,
+                               pred, row);
+                return cuda_check("sweep launch");
+            }
+        } else if (fold) {
+            return fail(KPL_EUNSUPPORTED, "deferred fold: iteration sweeps only");
+        }
         if (L.vx == 2)
             launch_pdl(stencil_sweep<2, In, Body>, grid, NT, 0, st, g, L, in, body, ws, cfg, phase, pred, row);
         else
@@ -398,6 +412,14 @@ void tma_prepare() {
     cudaFuncSetAttribute(tma_sweep<Body, tma_depth2<Body, true>(), PCIN, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)TmaRing<tma_depth2<Body, true>(), Body::kTmaStreams, true>::bytes());
+    if constexpr (is_pcg_iter<Body>::value) {        // the deferred-fold variants (multi-GPU)
+        cudaFuncSetAttribute(tma_sweep<Body, tma_depth2<Body, false>(), PCIN, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TmaRing<tma_depth2<Body, false>(), Body::kTmaStreams, false>::bytes());
+        cudaFuncSetAttribute(tma_sweep<Body, tma_depth2<Body, true>(), PCIN, true, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TmaRing<tma_depth2<Body, true>(), Body::kTmaStreams, true>::bytes());
+    }
     cudaGetLastError();
 }
 
@@ -466,6 +488,22 @@ int launch_tma(const kpl_op *op, const Layout &L, const double *in0, const doubl
     if (!ok) return fail(KPL_ECUDA, "cuTensorMapEncodeTiled failed");
     SGeo g{op->nx, op->ny, op->nz, op->diag, nullptr, nullptr, op->zhalo};
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    const bool fold = ws.px && ws.wait_epoch;
+    if constexpr (is_pcg_iter<Body>::value) {
+        if (fold) {
+            if (two_d)
+                launch_pdl(tma_sweep<Body, DEPTH2, PCIN, true, true>, (unsigned)L.items, NT + 32,
+                           TmaRing<DEPTH2, NSTR, true>::bytes(), st, maps, g, L, body, ws, cfg, phase, pred, row,
+                           wsel, zext, op->pc_const);
+            else
+                launch_pdl(tma_sweep<Body, DEPTH, PCIN, false, true>, (unsigned)L.items, NT + 32,
+                           TmaRing<DEPTH, NSTR, false>::bytes(), st, maps, g, L, body, ws, cfg, phase, pred, row,
+                           wsel, zext, op->pc_const);
+            return cuda_check("tma sweep launch");
+        }
+    } else if (fold) {
+        return fail(KPL_EUNSUPPORTED, "deferred fold: iteration sweeps only");
+    }
     if (two_d)
         launch_pdl(tma_sweep<Body, DEPTH2, PCIN, true>, (unsigned)L.items, NT + 32,
                    TmaRing<DEPTH2, NSTR, true>::bytes(), st, maps, g, L, body, ws, cfg, phase, pred, row, wsel, zext,

@@ -223,19 +223,23 @@ __device__ __forceinline__ void stencil_pass(const SGeo &g, const Layout &L, In 
     }
 }
 
-template <int VX, class In, class Body>
+template <int VX, class In, class Body, bool FOLD = false>
 __global__ void __launch_bounds__(NT, 2)
-stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws_in, Cfg cfg, int phase, int pred, long long row) {
+stencil_sweep(SGeo g, Layout L, In in, Body body, Ws ws, Cfg cfg, int phase, int pred, long long row) {
     __shared__ __align__(16) double sp[Body::kStencil ? 2 * SMEM_PLANE : 2];
     __shared__ double sred[NQ * NWARP];
-    __shared__ FoldSmem fsm;
     pdl_wait();
     pdl_launch_dependents();
-    const bool fold = ws_in.px && ws_in.wait_epoch;
-    if (fold) peer_fold_start(ws_in, cfg, fsm, sred);      // deferred fold of the previous sweep
-    const Ws ws = ws_fold_view(ws_in, &fsm.head, fsm.row, fold);
-    if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
-    stencil_pass<VX, In, Body>(g, L, in, body, ws, cfg, phase, sp, sred);
+    if constexpr (FOLD) {                                   // deferred fold of the previous sweep
+        __shared__ FoldSmem fsm;
+        peer_fold_start(ws, cfg, fsm, sred);
+        const Ws view = ws_fold_view(ws, &fsm.head, fsm.row, true);
+        if (!pred_ok(view.head, pred, row)) { peer_signal_idle(view); return; }
+        stencil_pass<VX, In, Body>(g, L, in, body, view, cfg, phase, sp, sred);
+    } else {
+        if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
+        stencil_pass<VX, In, Body>(g, L, in, body, ws, cfg, phase, sp, sred);
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -103,10 +103,10 @@ struct TmaRing {
 // only (the stencil input is used raw).
 // PCIN: transform of the stencil input -- 0 raw (m = w), 1 constant-diagonal
 // Jacobi (m = w * cin, precond.py:88-89 with inv_diag == cin).
-template <class Body, int D, int PCIN = 0, bool TWO_D = false>
-__global__ void __launch_bounds__(NT + 32, 2)
-tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws ws_in, Cfg cfg, int phase,
-          int pred, long long row, int wsel, int wzoff, double cin) {
+template <class Body, int D, int PCIN, bool TWO_D>
+__device__ __forceinline__ void tma_sweep_impl(const TmaMaps &maps, const SGeo &g, const Layout &L, Body &body,
+                                               const Ws &ws, const Cfg &cfg, int phase, int pred, long long row,
+                                               int wsel, int wzoff, double cin, double *sred) {
     using S = TmaShape<TWO_D>;
     constexpr int NSTR = Body::kTmaStreams;
     constexpr int SW = TmaRing<D, NSTR, TWO_D>::SW, SS = TmaRing<D, NSTR, TWO_D>::SS;
@@ -121,14 +121,7 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
     unsigned long long *sfull = wfull + SW;
     unsigned long long *wempty = sfull + SS;
     unsigned long long *sempty = wempty + SW;
-    __shared__ double sred[NQ * NWARP];
-    __shared__ FoldSmem fsm;
 
-    pdl_wait();
-    pdl_launch_dependents();
-    const bool fold = ws_in.px && ws_in.wait_epoch;
-    if (fold) peer_fold_start(ws_in, cfg, fsm, sred);      // deferred fold of the previous sweep
-    const Ws ws = ws_fold_view(ws_in, &fsm.head, fsm.row, fold);
     if (!pred_ok(ws.head, pred, row)) { peer_signal_idle(ws); return; }
     body.setup(ws);
     const long long par = wsel ? (ws.head->iter & 1) : 0;    // w_in = w[iter & 1] (ping-pong) or fixed
@@ -265,6 +258,26 @@ tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws 
             for (int q = 0; q < Q; ++q) ws.items[item * NQ + q] = t[q];
         }
         complete_item<Q>(ws, cfg, L, phase, c, sred);
+    }
+}
+
+// FOLD: the deferred fold of the previous sweep's peer exchange (kpl_sweep_peer
+// with wait_epoch) runs first and the sweep reads its scalars from the CTA's
+// private head; without it the body works on the kernel parameter directly.
+template <class Body, int D, int PCIN = 0, bool TWO_D = false, bool FOLD = false>
+__global__ void __launch_bounds__(NT + 32, 2)
+tma_sweep(const __grid_constant__ TmaMaps maps, SGeo g, Layout L, Body body, Ws ws, Cfg cfg, int phase,
+          int pred, long long row, int wsel, int wzoff, double cin) {
+    __shared__ double sred[NQ * NWARP];
+    pdl_wait();
+    pdl_launch_dependents();
+    if constexpr (FOLD) {
+        __shared__ FoldSmem fsm;
+        peer_fold_start(ws, cfg, fsm, sred);
+        const Ws view = ws_fold_view(ws, &fsm.head, fsm.row, true);
+        tma_sweep_impl<Body, D, PCIN, TWO_D>(maps, g, L, body, view, cfg, phase, pred, row, wsel, wzoff, cin, sred);
+    } else {
+        tma_sweep_impl<Body, D, PCIN, TWO_D>(maps, g, L, body, ws, cfg, phase, pred, row, wsel, wzoff, cin, sred);
     }
 }
 

@@ -351,5 +351,101 @@ def to_device_f64(v, n, device, what):
     a = np.asarray(v, dtype=np.float64)
     if a.shape != (n,):
         raise ValueError(f"{what} dimension mismatch")
-    host = t.from_numpy(np.ascontiguousarray(a))
-    return host.to(device, non_blocking=False), "numpy"
+    a = np.ascontiguousarray(a)
+    if a.nbytes >= _STAGE_MIN:
+        out = t.empty(n, dtype=t.float64, device=device)
+        _staging(device).h2d(a, out)
+        return out, "numpy"
+    return t.from_numpy(a).to(device, non_blocking=False), "numpy"
+
+
+def to_numpy_f64(d):
+    """Device fp64 vector -> a new numpy array (pipelined pinned staging when large)."""
+    if d.numel() * 8 >= _STAGE_MIN:
+        out = np.empty(d.numel(), dtype=np.float64)
+        _staging(d.device).d2h(d, out)
+        return out
+    return d.cpu().numpy()
+
+
+# Host <-> device copies of large numpy vectors (a kpl caller's b and x): a
+# pageable cudaMemcpy stages through one driver buffer at a time; here a ring
+# of pinned chunks is filled / drained by host threads (numpy copies release
+# the GIL) while the DMA engine moves the previous chunk, so the CPU memcpy
+# and the PCIe transfer overlap.
+_STAGE_MIN = 64 << 20          # below this the plain copy is as fast
+_STAGE_CHUNK = 16 << 20        # bytes per pinned slot
+_STAGE_SLOTS = 4
+_stagers: dict = {}
+
+
+def _staging(device):
+    key = str(device)
+    st = _stagers.get(key)
+    if st is None:
+        st = _stagers[key] = _HostStaging(device)
+    return st
+
+
+class _HostStaging:
+    def __init__(self, device):
+        import concurrent.futures
+        t = torch()
+        self.device = device
+        per = _STAGE_CHUNK // 8
+        self.slots = [t.empty(per, dtype=t.float64, pin_memory=True) for _ in range(_STAGE_SLOTS)]
+        self.views = [s.numpy() for s in self.slots]
+        self.events = [None] * _STAGE_SLOTS
+        self.pool = concurrent.futures.ThreadPoolExecutor(max_workers=_STAGE_SLOTS)
+        self.per = per
+
+    def h2d(self, a, out):
+        """out[:] = a (numpy, contiguous) on the current stream."""
+        t = torch()
+        stream = t.cuda.current_stream(self.device)
+        n, per = a.size, self.per
+        starts = list(range(0, n, per))
+        fill = lambda i, k0: np.copyto(self.views[i][:min(per, n - k0)], a[k0:k0 + per])
+        pending = {}
+        for j, k0 in enumerate(starts[:_STAGE_SLOTS]):
+            pending[j] = self.pool.submit(fill, j % _STAGE_SLOTS, k0)
+        for j, k0 in enumerate(starts):
+            i = j % _STAGE_SLOTS
+            pending.pop(j).result()
+            m = min(per, n - k0)
+            out[k0:k0 + m].copy_(self.slots[i][:m], non_blocking=True)
+            ev = t.cuda.Event()
+            ev.record(stream)
+            self.events[i] = ev
+            nxt = j + _STAGE_SLOTS
+            if nxt < len(starts):           # refill slot i once its DMA has left it
+                def refill(i=i, k0=starts[nxt], ev=ev):
+                    ev.synchronize()
+                    fill(i, k0)
+                pending[nxt] = self.pool.submit(refill)
+        for ev in self.events:
+            if ev is not None:
+                ev.synchronize()            # the caller may reuse `a` right away
+
+    def d2h(self, d, out):
+        """out[:] = d (device, contiguous) -- waits for the current stream's work on d."""
+        t = torch()
+        stream = t.cuda.current_stream(self.device)
+        n, per = d.numel(), self.per
+        starts = list(range(0, n, per))
+        drains = []
+        for j, k0 in enumerate(starts):
+            i = j % _STAGE_SLOTS
+            if j >= _STAGE_SLOTS:
+                drains[j - _STAGE_SLOTS].result()      # slot i's previous chunk is out
+            m = min(per, n - k0)
+            self.slots[i][:m].copy_(d[k0:k0 + m], non_blocking=True)
+            ev = t.cuda.Event()
+            ev.record(stream)
+
+            def drain(i=i, k0=k0, m=m, ev=ev):
+                ev.synchronize()
+                np.copyto(out[k0:k0 + m], self.views[i][:m])
+            drains.append(self.pool.submit(drain))
+        for f in drains:
+            f.result()

@@ -29,7 +29,7 @@ def spmv(A, v):
     out = D.torch().empty(dm.n, dtype=vd.dtype, device=dev)
     op = D.make_op(dm)
     _lib.check(_lib.load().kpl_spmv(op, D.ptr(vd), D.ptr(out), D.stream_handle()), "spmv")
-    return out.cpu().numpy() if host == "numpy" else (out.cpu() if host else out)
+    return D.to_numpy_f64(out) if host == "numpy" else (out.cpu() if host else out)
 
 
 def _dot_dev(op, ud, vd, dev):
@@ -67,7 +67,7 @@ def axpy(alpha, x, y):
     out = D.torch().empty_like(yd)
     _lib.check(_lib.load().kpl_axpy(n, float(alpha), D.ptr(xd), D.ptr(yd), D.ptr(out),
                                     D.stream_handle()), "axpy")
-    return out.cpu().numpy() if host == "numpy" else (out.cpu() if host else out)
+    return D.to_numpy_f64(out) if host == "numpy" else (out.cpu() if host else out)
 
 
 def precond_apply(M, v):
@@ -98,4 +98,4 @@ def precond_apply(M, v):
     out = t.empty_like(vd)
     _lib.check(lib.kpl_precond_apply(op, D.ptr(vd), D.ptr(out), D.ptr(ws), D.stream_handle()),
                "preconditioner apply")
-    return out.cpu().numpy() if host == "numpy" else (out.cpu() if host else out)
+    return D.to_numpy_f64(out) if host == "numpy" else (out.cpu() if host else out)

@@ -362,7 +362,7 @@ class _Solve:
             raw = self.ws[self.reps_off:self.reps_off + 8 * int(st.n_replacements)]
             reps = [int(v) for v in raw.view(t.int64).cpu().numpy()]
         if self.host_io == "numpy":
-            x = self.x.cpu().numpy()
+            x = D.to_numpy_f64(self.x)
         elif self.host_io == "host":
             t = D.torch()
             x = t.empty(self.n, dtype=t.float64, pin_memory=True)

@@ -127,3 +127,22 @@ def test_lazy_replacement_equals_eager(monkeypatch, form, with_callback):
                (c.alpha, c.beta, c.gamma, c.delta, c.rnorm_recursive, c.rnorm_true)
     assert np.asarray(e.x).tobytes() == np.asarray(l.x).tobytes()
     assert se == sl
+
+
+@gpu
+@pytest.mark.parametrize("n", [8_388_608 + 1, 25_000_003])
+def test_pipelined_host_staging_round_trip(n):
+    """Large numpy b / x (a kpl caller's types) go through the pinned staging ring
+    (device.to_device_f64 / to_numpy_f64): every byte must arrive, ragged tail
+    chunk included."""
+    _need_gpu()
+    import torch
+    from paper_1706_05988_b200 import device as D
+    a = np.random.default_rng(n).standard_normal(n)
+    a[::7] = -0.0
+    d, io = D.to_device_f64(a, n, D.require_cuda(), "vector")
+    assert io == "numpy"
+    assert d.cpu().numpy().tobytes() == a.tobytes()
+    back = D.to_numpy_f64(d * 1.0)
+    assert back.tobytes() == a.tobytes()
+    torch.cuda.synchronize()

@@ -35,8 +35,9 @@ REF = {  # (iterations, final true relative residual)
     ("1", "pcg_sh"): (450, 9.466e-13), ("1", "pcg_rr"): (450, 9.55e-13),
     ("2", "cg"): (4764, 9.949e-11), ("2", "pcg"): (4764, 7.607e-10),
     ("2", "pcg_sh"): (4764, 9.949e-11),
-    ("5", "cg"): (88, 5.746e-11), ("5", "pcg"): (88, 5.758e-11),
-    ("5", "pcg_sh"): (88, 5.746e-11), ("5", "pcg_rr"): (88, 5.746e-11),
+    # config 5: the unmodified reference's kpl.solve on the same arrays (profiles/r02_reference_cpu.jsonl)
+    ("5", "cg"): (88, 4.551026644281697e-11), ("5", "pcg"): (88, 4.5673596921911305e-11),
+    ("5", "pcg_sh"): (88, 4.551026657642009e-11), ("5", "pcg_rr"): (88, 4.551026319857749e-11),
     # config 4 (256^3): the full-size oracle in the reference order (tests/golden/config4_oracle_*.npz,
     # tools/oracle_fullsize.py); the sigma* = 0.49238826317067413 of the rule at 256^3
     # (profiles/r02_sigma_config4.jsonl) -- every sigma > 0 of the sweep is held to CG's target

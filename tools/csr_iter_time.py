@@ -1,6 +1,6 @@
 """Device time of N p-CG-sh iteration sweeps (no result check) -- A/B timing helper.
 
-    KPL_CSR_GATHER=csr|sorted KPL_SORTED_NT=256|512|1024 python tools/csr_iter_time.py [c2c,c4,c5]
+    KPL_CSR_GATHER=csr|sorted KPL_SORTED_NT=256|512|1024 python tools/csr_iter_time.py [c2c,c4,c5] [chunk_blocks]
 
 Matrices are cached under /tmp/kpl_cache (generation of config 5 takes ~30 s).
 """
@@ -41,12 +41,14 @@ def matrix(name):
 
 def main():
     names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c2c", "c4", "c5"]
-    tag = f"gather={os.environ.get('KPL_CSR_GATHER', 'auto')} nt={os.environ.get('KPL_SORTED_NT', '512')}"
+    cb = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    tag = (f"gather={os.environ.get('KPL_CSR_GATHER', 'csr')} nt={os.environ.get('KPL_SORTED_NT', '512')} "
+           f"chunk_blocks={cb or 'default'}")
     for name in names:
         A = matrix(name)
         M = K.make_jacobi(A)
         b = torch.as_tensor(RHS[name](A.n), device="cuda")
-        S = _Solve(A, M, b, None, K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=100))
+        S = _Solve(A, M, b, None, K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=100), chunk_blocks=cb)
         S.init()
         S.iterate(1)
         torch.cuda.synchronize()
@@ -58,7 +60,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             best = min(best, e0.elapsed_time(e1) / 9)
-            S = _Solve(A, M, b, None, K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=100))
+            S = _Solve(A, M, b, None, K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=100), chunk_blocks=cb)
             S.init()
             S.iterate(1)
             torch.cuda.synchronize()
