@@ -112,6 +112,29 @@ typedef struct kpl_op {
     const uint16_t *sp_dest;
     int32_t sp_rows;
     int32_t sp_max;
+    /* CSR, optional shared-memory-window layout of the SpMV for scattered
+       banded matrices (NULL = not used; takes precedence over sp_*).  Rows are
+       grouped in super-blocks of 1024*bd_rpt rows, one CTA each.  Super-block s
+       walks its column span in bd_sb[4s+1] windows of bd_w columns starting at
+       column bd_sb[4s+2] (even); window j of super-block s is "pass"
+       p = bd_sb[4s] + j, and the CTA holds the window's slice of the input
+       vector in shared memory (bulk copies, double-buffered), so the gathers
+       are shared-memory loads.  Inside a pass the rows come in groups of 32
+       (group g = rows 32g..32g+31 of the super-block); bd_len[p*RB + t] is the
+       number of nonzeros of local row t inside the window (<= 255) and the
+       group's nonzeros start at bd_grp[p*RB/32 + g] (one terminal entry at the
+       end), stored in jagged-diagonal order: step k of every row that has one,
+       in lane order.  bd_val / bd_col hold the values and the columns relative
+       to the window start (uint16).  Lane l sums row l's products left to
+       right across the passes, i.e. in ascending column order from +0.0: the
+       csr_matvec order (_kernels.py:44-52), bit for bit.                      */
+    const double   *bd_val;
+    const uint16_t *bd_col;
+    const uint8_t  *bd_len;
+    const int32_t  *bd_grp;
+    const int32_t  *bd_sb;
+    int32_t bd_rpt;          /* 1..8: rows per super-block / 1024                 */
+    int32_t bd_w;            /* window length in columns (even, <= 65536)         */
 } kpl_op;
 
 #define KPL_ORDER_TREE      0

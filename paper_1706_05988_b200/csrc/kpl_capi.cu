@@ -22,6 +22,7 @@
 #include "kpl_ic0.cuh"
 #include "kpl_peer.cuh"
 #include "kpl_spmv_tma.cuh"
+#include "kpl_spmv_band.cuh"
 
 using namespace kpl;
 
@@ -93,6 +94,10 @@ int make_layout(const kpl_op *op, Layout &L) {
         if (op->sp_col && (!op->sp_val || !op->sp_dest || op->sp_rows < 1 || op->sp_max < 1 ||
                            op->sp_max > 65535 || 8LL * op->sp_max > 227 * 1024))
             return fail(KPL_EINVAL, "bad column-sorted SpMV layout");
+        if (op->bd_val && (!op->bd_col || !op->bd_len || !op->bd_grp || !op->bd_sb || op->bd_rpt < 1 ||
+                           op->bd_rpt > 8 || op->bd_w < 2 || (op->bd_w & 1) || op->bd_w > 65536 ||
+                           16LL * op->bd_w + 64 > 227 * 1024))
+            return fail(KPL_EINVAL, "bad window SpMV layout");
         L.vx = 1; L.wx = NWARP; L.wy = 1; L.zc = cb;
         L.T = cb;
         L.items = blocks;
@@ -282,6 +287,52 @@ void launch_sorted(const kpl_op *op, const CGeo &g, const SIn &in, double *out, 
     }
 }
 
+// Shared-memory-window SpMV (kpl_op.bd_*): one CTA per super-block of 1024*bd_rpt
+// rows, 16*bd_w bytes of dynamic shared memory (two input windows).  Taken for
+// plain vector inputs whose storage allows 16-byte bulk copies; anything else
+// (classic CG's p = beta*p + u evaluated on the fly, a Jacobi diagonal gathered
+// per column) keeps the CSR-order kernels.
+template <class SIn> struct band_capable : std::false_type {};
+template <> struct band_capable<InVec<KPL_PC_IDENTITY, 0>> : std::true_type {};
+
+template <class SIn>
+bool band_ok(const kpl_op *op, const SIn &in) {
+    if constexpr (band_capable<SIn>::value) {
+        return op->bd_val && op->chunks_global <= 0 && !((reinterpret_cast<uintptr_t>(in.a0) | reinterpret_cast<uintptr_t>(in.a1)) & 15);
+    } else {
+        return false;
+    }
+}
+
+template <class SIn, int RPT>
+void launch_band_rpt(const kpl_op *op, const BandGeo &bg, const SIn &in, double *out, const Ws &ws, int pred,
+                     long long row, cudaStream_t st) {
+    auto kern = csr_band_spmv<SIn, RPT, 2>;
+    const size_t smem = 16 * (size_t)op->bd_w + 64;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned grid = (unsigned)cdiv(op->n, 1024LL * RPT);
+    launch_pdl(kern, grid, 1024, smem, st, (long long)op->n, bg, in, out, ws, pred, row);
+}
+
+template <class SIn>
+void launch_band(const kpl_op *op, const SIn &in, double *out, const Ws &ws, int pred, long long row,
+                 cudaStream_t st) {
+    if constexpr (band_capable<SIn>::value) {
+        const BandGeo bg{op->bd_val, op->bd_col, op->bd_len, op->bd_grp, reinterpret_cast<const int4 *>(op->bd_sb),
+                         op->bd_w};
+        switch (op->bd_rpt) {
+        case 1: launch_band_rpt<SIn, 1>(op, bg, in, out, ws, pred, row, st); break;
+        case 2: launch_band_rpt<SIn, 2>(op, bg, in, out, ws, pred, row, st); break;
+        case 3: launch_band_rpt<SIn, 3>(op, bg, in, out, ws, pred, row, st); break;
+        case 4: launch_band_rpt<SIn, 4>(op, bg, in, out, ws, pred, row, st); break;
+        case 5: launch_band_rpt<SIn, 5>(op, bg, in, out, ws, pred, row, st); break;
+        case 6: launch_band_rpt<SIn, 6>(op, bg, in, out, ws, pred, row, st); break;
+        case 7: launch_band_rpt<SIn, 7>(op, bg, in, out, ws, pred, row, st); break;
+        default: launch_band_rpt<SIn, 8>(op, bg, in, out, ws, pred, row, st); break;
+        }
+    }
+}
+
 // CSR-order SpMV: KPL_SPMV=plain keeps the one-window-at-a-time kernel for A/B
 // runs; the default pipelines the next window's loads under the row sums.
 template <class SIn>
@@ -341,7 +392,14 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
             // short rows (structured matrices): gathers L2-direct (configs 2-CSR, 4: -4 %); long
             // scattered rows keep the read-only path (ld.global.nc is 3 % faster on config 5)
             const bool long_rows = op->nnz > 16 * op->n;
-            if (op->sp_col) {
+            bool band = false;
+            if constexpr (std::is_same<SpIn, NoSpmvIn>::value) band = band_ok(op, in);
+            else band = band_ok(op, spin);
+            if (band) {
+                // scattered band: input windows in shared memory, one CTA per super-block
+                if constexpr (std::is_same<SpIn, NoSpmvIn>::value) launch_band(op, in, ws.nbuf, ws, pred, row, st);
+                else launch_band(op, spin, ws.nbuf, ws, pred, row, st);
+            } else if (op->sp_col) {
                 // column-sorted gathers (scattered matrices): one CTA per block of sp_rows rows
                 if constexpr (std::is_same<SpIn, NoSpmvIn>::value) launch_sorted(op, g, in, ws.nbuf, ws, pred, row, st);
                 else launch_sorted(op, g, spin, ws.nbuf, ws, pred, row, st);
@@ -637,7 +695,9 @@ int kpl_spmv(const kpl_op *op, const double *v, double *out, void *stream) {
     if (op->kind == KPL_OP_CSR) {
         CGeo g{op->n, op->row_ptr, op->col_idx, op->values};
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        if (op->sp_col)
+        if (band_ok(op, in) && !(reinterpret_cast<uintptr_t>(v) & 15))
+            launch_band(op, in, out, ws, PRED_ALWAYS, 0, (cudaStream_t)stream);
+        else if (op->sp_col)
             launch_sorted(op, g, in, out, ws, PRED_ALWAYS, 0, (cudaStream_t)stream);
         else
             csr_spmv_kernel<InVec<KPL_PC_IDENTITY>><<<(unsigned)L.items, NT, 0, (cudaStream_t)stream>>>(

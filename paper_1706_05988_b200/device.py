@@ -104,6 +104,7 @@ class DeviceMatrix:
             self.row_ptr = self.col_idx = self.values = None
             self.nnz = 0
             self.sorted = None
+            self.band = None
         else:
             self.kind = _lib.KPL_OP_CSR
             nnz = len(A.values)
@@ -115,7 +116,115 @@ class DeviceMatrix:
             self.nnz = nnz
             self.nx = self.ny = self.nz = 0
             self.diag = 0.0
-            self.sorted = sorted_gather_layout(A.row_ptr, A.col_idx, self.row_ptr, self.col_idx, self.values)
+            self.band = band_layout(A.row_ptr, A.col_idx, self.row_ptr, self.col_idx, self.values)
+            self.sorted = None if self.band is not None else sorted_gather_layout(
+                A.row_ptr, A.col_idx, self.row_ptr, self.col_idx, self.values)
+
+
+def gather_mode():
+    """KPL_CSR_GATHER: how the CSR SpMV reads its input vector.
+    auto (default) -- the shared-memory-window layout (kpl_op.bd_*) for scattered
+    banded matrices that qualify, CSR-order gathers otherwise; band -- the window
+    layout whenever it can be built; sorted -- the column-sorted layout
+    (kpl_op.sp_*); csr -- always gather in CSR order."""
+    mode = os.environ.get("KPL_CSR_GATHER", "auto")
+    if mode not in ("auto", "csr", "sorted", "band"):
+        raise ValueError(f"KPL_CSR_GATHER={mode!r}: expected auto, csr, sorted or band")
+    return mode
+
+
+# Shared-memory-window SpMV (kpl_op.bd_*, csrc/kpl_spmv_band.cuh).  Two windows
+# of the input vector live in shared memory: 16 bytes per window column.
+_BAND_W_MAX = 14336                  # 2 x 112 KiB of the 227 KiB a CTA may use
+_BAND_MIN_LINES = 12.0               # auto: CSR-order warp gathers touching >= 12 lines ...
+_BAND_MIN_ROW_NNZ = 16.0             # ... on rows longer than 16 nonzeros on average
+_BAND_MAX_LEN_BYTES = 0.25           # the per-(row, pass) length bytes stay under 25 % of the 10 B/nnz stream
+_SMS = 148
+
+
+def band_rows_per_thread(n):
+    """Super-block height / 1024: the value in 4..7 whose CTA count fills whole
+    waves of 148 SMs best (ties: the taller block); small matrices: one wave."""
+    if n <= 4 * 1024 * _SMS:
+        return max(1, min(4, -(-n // (1024 * _SMS))))
+    best = None
+    for rpt in (7, 6, 5, 4):
+        nsb = -(-n // (1024 * rpt))
+        eff = nsb / (-(-nsb // _SMS) * _SMS)
+        if best is None or eff > best[0] + 1e-12:
+            best = (eff, rpt)
+    return best[1]
+
+
+def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, window=None, rpt=None):
+    """(bd_val, bd_col, bd_len, bd_grp, bd_sb, rpt, W) or None -- the layout
+    include/kpl_b200.h documents under kpl_op.bd_*.  Index work only (values are
+    permuted, never combined), done once per matrix with torch sorts on the
+    device the CSR arrays live on."""
+    mode = gather_mode() if mode is None else mode
+    if mode in ("csr", "sorted"):
+        return None
+    t = torch()
+    n = int(row_ptr.numel()) - 1
+    nnz = int(col_idx.numel())
+    if n < 1 or nnz < 1:
+        return None
+    if mode == "auto" and (nnz < _BAND_MIN_ROW_NNZ * n or csr_lines_per_warp(col_idx_h) < _BAND_MIN_LINES):
+        return None
+    W = int(window or os.environ.get("KPL_BAND_W", _BAND_W_MAX))
+    if W < 2 or W % 2 or W > _BAND_W_MAX:
+        raise ValueError(f"window SpMV: window length {W} (expected an even value in 2..{_BAND_W_MAX})")
+    rpt = int(rpt or int(os.environ.get("KPL_BAND_RPT", 0)) or band_rows_per_thread(n))
+    if not 1 <= rpt <= 8:
+        raise ValueError("window SpMV: rows per thread must be in 1..8")
+    RB = 1024 * rpt
+    G = RB // 32
+    nsb = -(-n // RB)
+    dev = row_ptr.device
+    counts = (row_ptr[1:] - row_ptr[:-1]).long()
+    rows = t.repeat_interleave(t.arange(n, device=dev), counts)
+    sb = rows // RB
+    col = col_idx.long()
+    big = t.iinfo(t.int64).max
+    c_lo = t.full((nsb,), big, dtype=t.int64, device=dev).scatter_reduce_(0, sb, col, "amin", include_self=True)
+    c_hi = t.full((nsb,), -1, dtype=t.int64, device=dev).scatter_reduce_(0, sb, col, "amax", include_self=True)
+    c_lo = t.where(c_hi < 0, t.zeros_like(c_lo), c_lo) & ~1          # even: 16-byte bulk copies
+    c_hi = t.clamp(c_hi, min=0)
+    npass = (c_hi - c_lo) // W + 1
+    pass0 = t.cumsum(npass, 0) - npass
+    NP = int(npass.sum())
+    if mode == "auto" and NP * RB > _BAND_MAX_LEN_BYTES * 10.0 * nnz:
+        return None                                                   # too wide a span for the window walk
+    if NP * RB >= 2**31 or NP * G + 1 >= 2**31:
+        return None
+    rel = col - c_lo[sb]
+    j = rel // W
+    p = pass0[sb] + j
+    bcol = rel - j * W
+    # (pass, local row) lengths; CSR order is (row, column) and j grows with the column,
+    # so a stable sort by the (pass, group, step, lane) key needs the entry's rank inside
+    # its (pass, row) segment
+    slot = p * RB + (rows - sb * RB)
+    lens = t.bincount(slot, minlength=NP * RB)
+    if int(lens.max()) > 255:
+        return None
+    order = t.argsort(slot, stable=True)                              # (pass, row, column)
+    seg_start = t.cumsum(lens, 0) - lens
+    k = t.empty_like(order)
+    k[order] = t.arange(nnz, device=dev) - seg_start[slot[order]]
+    lrow = rows - sb * RB
+    key = ((p * G + lrow // 32) * 256 + k) * 32 + lrow % 32
+    perm = t.argsort(key)
+    del key, k, order, seg_start, slot
+    pad = lambda a: t.cat([a, a.new_zeros(8)])
+    bd_val = pad(values[perm])
+    bd_col = pad(bcol[perm].to(t.int32).to(t.int16))                  # < 65536: uint16 bits
+    bd_len = lens.to(t.uint8)
+    gtot = lens.view(NP * G, 32).sum(1)
+    bd_grp = t.zeros(NP * G + 1, dtype=t.int32, device=dev)
+    bd_grp[1:] = t.cumsum(gtot, 0).to(t.int32)
+    bd_sb = t.stack([pass0, npass, c_lo, t.zeros_like(c_lo)], 1).to(t.int32).contiguous()
+    return bd_val, bd_col, bd_len, bd_grp, bd_sb, rpt, W
 
 
 # Column-sorted SpMV gathers (kpl_op.sp_*): meant for matrices whose CSR-order
@@ -145,10 +254,7 @@ def sorted_gather_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values):
     """(sp_col, sp_val, sp_dest, rows per block, max block nnz) or None.  Index
     work only (the values are permuted, never combined), done once per matrix
     with device sorts."""
-    mode = os.environ.get("KPL_CSR_GATHER", "csr")
-    if mode not in ("auto", "csr", "sorted"):
-        raise ValueError(f"KPL_CSR_GATHER={mode!r}: expected auto, csr or sorted")
-    if mode == "csr" or (mode == "auto" and csr_lines_per_warp(col_idx_h) < _SORTED_MIN_LINES):
+    if gather_mode() != "sorted":
         return None
     rp = np.asarray(row_ptr_h, dtype=np.int64)
     n = len(rp) - 1
@@ -308,6 +414,10 @@ def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk
             sc, sv, sd, R, most = dm.sorted
             op.sp_col, op.sp_val, op.sp_dest = ptr(sc), ptr(sv), ptr(sd)
             op.sp_rows, op.sp_max = R, most
+        if dm.band is not None:
+            bv, bc, bl, bg, bs, rpt, W = dm.band
+            op.bd_val, op.bd_col, op.bd_len, op.bd_grp, op.bd_sb = ptr(bv), ptr(bc), ptr(bl), ptr(bg), ptr(bs)
+            op.bd_rpt, op.bd_w = rpt, W
     op.zc = zc
     op.vx = vx
     op.chunk_blocks = chunk_blocks

@@ -79,7 +79,10 @@ CASES = [
     ("register", lambda: (K.Stencil3D(33, 9, 20), None), dict(method="pcg_rr"), {}),
     ("persistent", lambda: (K.Stencil2D(60, 50), None), dict(method="pcg_sh", shift=2.0), {}),
     ("csr_window", lambda: (problems.varcoef_3d(11, seed=1), "jacobi"), dict(method="pcg_sh", shift=0.5), {}),
-    ("csr_pipe", lambda: (problems.banded_spd(20_000, seed=2, band=3000), "jacobi"), dict(method="pcg_rr"), {}),
+    ("csr_pipe", lambda: (problems.banded_spd(20_000, seed=2, band=3000), "jacobi"), dict(method="pcg_rr"),
+     {"env": ("KPL_CSR_GATHER", "csr")}),
+    ("csr_band", lambda: (problems.banded_spd(20_001, seed=2, band=3000), "jacobi"), dict(method="pcg_rr"),
+     {"env": ("KPL_CSR_GATHER", "band"), "env2": ("KPL_BAND_W", "1022")}),
     ("csr_sorted", lambda: (problems.banded_spd(20_000, seed=2, band=3000), "jacobi"),
      dict(method="pcg_sh", shift=0.4), {"env": ("KPL_CSR_GATHER", "sorted")}),
     ("csr_sorted_plain", lambda: (problems.banded_spd(20_000, seed=2, band=3000), "jacobi"),

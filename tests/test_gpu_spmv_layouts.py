@@ -1,9 +1,10 @@
-"""The two CSR SpMV gather layouts give identical bits (needs a B200).
+"""The CSR SpMV gather layouts give identical bits (needs a B200).
 
 `KPL_CSR_GATHER=csr` gathers the input in CSR order (csr_spmv_kernel);
 `sorted` gathers it in column order per block of rows and sums each row in
-CSR order out of shared memory (csr_sorted_spmv).  Both must
-equal the oracle's csr_matvec (`_kernels.py:44-52`) bit for bit, and whole
+CSR order out of shared memory (csr_sorted_spmv); `band` walks
+shared-memory windows of the input per super-block of rows (csr_band_spmv,
+kpl_spmv_band.cuh).  All must equal the oracle's csr_matvec (`_kernels.py:44-52`) bit for bit, and whole
 solves must not change by a single bit when the layout changes.
 """
 
@@ -45,22 +46,44 @@ def test_spmv_layouts_bitwise(monkeypatch, name, make):
     v[1::7] = -0.0
     want = O.spmv(O.as_oracle_operator(A), v)
     outs = {}
-    for mode in ("csr", "sorted"):
+    for mode in ("csr", "sorted", "band"):
         monkeypatch.setenv("KPL_CSR_GATHER", mode)
         B = fresh(A)
         got = np.asarray(K.spmv(B, v))
         dm = D.device_matrix(B, D.require_cuda())
         assert (dm.sorted is not None) == (mode == "sorted")
+        # "rspd" is dense (300 nonzeros per row: a (row, window) segment over 255) -> no window layout
+        assert (dm.band is not None) == (mode == "band" and name != "rspd")
         assert same_bits(got, want), (mode, first_diff(got, want))
         outs[mode] = got
     assert same_bits(outs["csr"], outs["sorted"])
+    assert same_bits(outs["csr"], outs["band"])
 
 
-def test_auto_picks_sorted_for_scattered_only(monkeypatch):
-    monkeypatch.setenv("KPL_CSR_GATHER", "auto")
+@pytest.mark.parametrize("window,rpt", [(2, 1), (64, 1), (1000, 2), (4096, 3), (14336, 8), (14336, 0)])
+def test_band_windows_and_block_heights_bitwise(monkeypatch, window, rpt):
+    """Many short passes, odd window tails (n odd), every super-block height."""
+    monkeypatch.setenv("KPL_CSR_GATHER", "band")
+    monkeypatch.setenv("KPL_BAND_W", str(window))
+    monkeypatch.setenv("KPL_BAND_RPT", str(rpt))
+    A = problems.banded_spd(9_001 if window <= 64 else 70_001, seed=window, band=700 if window <= 64 else 30_000)
+    v = np.random.default_rng(11).standard_normal(A.n)
+    v[::3] = -0.0
+    want = O.spmv(O.as_oracle_operator(A), v)
+    B = fresh(A)
+    got = np.asarray(K.spmv(B, v))
+    lay = D.device_matrix(B, D.require_cuda()).band
+    assert lay is not None and lay[6] == window and (rpt == 0 or lay[5] == rpt)
+    assert same_bits(got, want), first_diff(got, want)
+
+
+def test_auto_picks_the_window_layout_for_scattered_only(monkeypatch):
+    monkeypatch.delenv("KPL_CSR_GATHER", raising=False)
     dev = D.require_cuda()
-    assert D.device_matrix(fresh(problems.banded_spd(40_000, seed=0)), dev).sorted is not None
-    assert D.device_matrix(fresh(K.laplacian_2d(300, 300)), dev).sorted is None
+    dm = D.device_matrix(fresh(problems.banded_spd(40_000, seed=0)), dev)
+    assert dm.band is not None and dm.sorted is None
+    dm = D.device_matrix(fresh(K.laplacian_2d(300, 300)), dev)
+    assert dm.band is None and dm.sorted is None
 
 
 @pytest.mark.parametrize("method,extra", [("pcg_sh", {"shift": 0.41}), ("cg", {}), ("pcg_rr", {})])
@@ -69,12 +92,13 @@ def test_solves_identical_across_layouts(monkeypatch, method, extra):
     b = np.random.default_rng(2).standard_normal(A.n)
     kw = dict(method=method, max_iters=60, rtol=1e-10, **extra)
     res = {}
-    for mode in ("csr", "sorted"):
+    for mode in ("csr", "sorted", "band"):
         monkeypatch.setenv("KPL_CSR_GATHER", mode)
         B = fresh(A)
         res[mode] = K.solve(B, K.make_jacobi(B), b, None, K.SolverConfig(**kw))
-    assert same_bits(hist6(res["csr"]), hist6(res["sorted"]))
-    assert same_bits(res["csr"].x, res["sorted"].x)
+    for mode in ("sorted", "band"):
+        assert same_bits(hist6(res["csr"]), hist6(res[mode])), mode
+        assert same_bits(res["csr"].x, res[mode].x), mode
     # and both are the oracle run in the device's reduction order
     ores = O.solve(A, O.make_jacobi(O.as_oracle_operator(A)), b, None, O.Config(**kw), dot=gpu_dot(A))
     assert same_bits(hist6(res["sorted"]), oracle_hist6(ores))

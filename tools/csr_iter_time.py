@@ -42,7 +42,7 @@ def matrix(name):
 def main():
     names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c2c", "c4", "c5"]
     cb = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-    tag = (f"gather={os.environ.get('KPL_CSR_GATHER', 'csr')} nt={os.environ.get('KPL_SORTED_NT', '512')} "
+    tag = (f"gather={os.environ.get('KPL_CSR_GATHER', 'auto')} nt={os.environ.get('KPL_SORTED_NT', '512')} "
            f"chunk_blocks={cb or 'default'}")
     for name in names:
         A = matrix(name)
