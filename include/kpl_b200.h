@@ -135,6 +135,13 @@ typedef struct kpl_op {
     const int32_t  *bd_sb;
     int32_t bd_rpt;          /* 1..8: rows per super-block / 1024                 */
     int32_t bd_w;            /* window length in columns (even, <= 65536)         */
+    /* most nonzeros in one round (32 consecutive groups of one pass); > 0
+       selects the ring-fed kernel, which streams bd_val/bd_col/bd_len/bd_grp
+       through shared memory with bulk copies when at least two ring slots of
+       this size fit next to the two windows.  The arrays then need 8 spare
+       entries (bd_val, bd_col) / 4 spare ints (bd_grp) of padding at the end. */
+    int32_t bd_round_max;
+    int32_t _reserved2;
 } kpl_op;
 
 #define KPL_ORDER_TREE      0

@@ -304,9 +304,31 @@ bool band_ok(const kpl_op *op, const SIn &in) {
     }
 }
 
+// ring slots that fit next to the two windows (0: the plain-load kernel)
+BandRing band_ring(const kpl_op *op) {
+    const char *e = std::getenv("KPL_BAND_KERNEL");       // read per launch: the tests switch it
+    const bool off = e && !std::strcmp(e, "ldg");
+    BandRing r{0, 0};
+    if (off || op->bd_round_max <= 0) return r;
+    r.cap = (op->bd_round_max + 16 + 63) / 64 * 64;
+    const long long room = 227LL * 1024 - 16LL * op->bd_w - 128;
+    r.ns = (int)std::min<long long>(4, room / (long long)r.slot());
+    if (r.ns < 2) r.ns = 0;
+    return r;
+}
+
 template <class SIn, int RPT>
 void launch_band_rpt(const kpl_op *op, const BandGeo &bg, const SIn &in, double *out, const Ws &ws, int pred,
                      long long row, cudaStream_t st) {
+    const BandRing ring = band_ring(op);
+    if (ring.ns) {
+        auto kern = csr_band_ring_spmv<SIn, RPT>;
+        const size_t smem = ring.bytes(op->bd_w);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const unsigned grid = (unsigned)cdiv(op->n, 1024LL * RPT);
+        launch_pdl(kern, grid, BAND_CW * 32 + 32, smem, st, (long long)op->n, bg, ring, in, out, ws, pred, row);
+        return;
+    }
     auto kern = csr_band_spmv<SIn, RPT, 2>;
     const size_t smem = 16 * (size_t)op->bd_w + 64;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

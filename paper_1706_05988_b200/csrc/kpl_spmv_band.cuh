@@ -131,4 +131,185 @@ csr_band_spmv(long long n, BandGeo B, In in, double *__restrict__ out, Ws ws, in
     }
 }
 
+// ---------------------------------------------------------------------------
+// Ring-fed form.  With ~224 KB of the SM's 256 KB carved out as shared memory
+// almost no L1 is left, and the value/column stream of csr_band_spmv (plain
+// loads) runs out of L1 miss slots long before it reaches the DRAM rate: the
+// kernel is latency-bound (ncu: 17 of 32 warps on the long scoreboard, DRAM at
+// 40 %).  Here the stream never touches the LSU's global path: a producer warp
+// moves it with cp.async.bulk into a ring of shared-memory slots, one slot per
+// "round" (32 consecutive groups of a pass: their values, columns, row lengths
+// and group offsets -- four contiguous slices of the bd_* arrays), and the 16
+// consumer warps (two groups of a round each) read values, columns and the
+// input window from shared memory only.  Same walk, same sums: bit-identical
+// to csr_band_spmv.
+//
+//   slot = | val[cap] | col[cap] | len[1024] | grp[36] |     cap % 64 == 0
+//   barriers: xfull[2] (input windows), full[ns] (1 arrival + bytes), empty[ns] (16 arrivals)
+//
+//   warp 16 (producer)                           warps 0..15 (consumers), thread t: rows t + 512 h + 1024 i
+//   ------------------------------------        ---------------------------------------------------------
+//   round boundaries 32 at a time (one per       per pass: wait the window; per round: wait full[slot],
+//   lane); per round: wait empty[slot],          walk groups w and w + 16 (two independent chains),
+//   expect_tx, 4 bulk copies                     arrive on empty[slot]; bar.sync among consumers, window j+2
+//
+// (A CTA cannot exceed 1024 threads.  Measured alternatives on config 5: all 32
+// warps consuming with the producer role rotating among them -- every round then
+// waits for the slowest warp, 0.51 ms/iteration -- or with warp 0 feeding the
+// ring between its own groups without blocking -- fills lag, 0.37; this form: 0.27.)
+struct BandRing {
+    int cap, ns;
+    __host__ __device__ size_t slot() const { return 10 * (size_t)cap + 1024 + 144; }
+    __host__ __device__ size_t bytes(int W) const { return 16 * (size_t)W + ns * slot() + 8 * (2 + 2 * (size_t)ns); }
+};
+
+// try_wait with a suspend-time hint: a waiting warp sleeps instead of spinning on the barrier word
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long *b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity), "r"(2000u)
+        : "memory");
+}
+
+constexpr int BAND_CW = 16;                        // consumer warps
+
+template <class In, int RPT>
+__global__ void __launch_bounds__(BAND_CW * 32 + 32, 1)
+csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict__ out, Ws ws, int pred,
+                   long long row) {
+    constexpr int RBS = RPT * 1024, G = RBS / 32, NC = BAND_CW * 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double *xs0 = reinterpret_cast<double *>(smem);
+    double *xs1 = xs0 + B.W;
+    unsigned char *ring = smem + 16 * (size_t)B.W;
+    const size_t SLOT = R.slot();
+    unsigned long long *xfull = reinterpret_cast<unsigned long long *>(ring + R.ns * SLOT);
+    unsigned long long *full = xfull + 2;
+    unsigned long long *empty = full + R.ns;
+    pdl_wait();
+    pdl_launch_dependents();
+    if (ws.head && !pred_ok(ws.head, pred, row)) return;
+    if (ws.head) in.setup(ws);
+    const double *x = in.base();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int4 info = __ldg(B.sb + blockIdx.x);
+    const int pass0 = info.x, npass = info.y;
+    if (tid == 0) {
+        mbar_init(&xfull[0], 1);
+        mbar_init(&xfull[1], 1);
+        for (int s = 0; s < R.ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], BAND_CW); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == BAND_CW) {
+        // ------------------------------------------------------------ producer
+        const int nq = npass * RPT;                    // rounds of this super-block
+        const long long g0 = (long long)pass0 * G;     // its first group
+        int s = 0, wrap = 0;
+        for (int qb = 0; qb < nq; qb += 32) {
+            // round boundaries of the next 32 rounds, one per lane
+            const int q = min(qb + lane, nq - 1);
+            const int eb = __ldg(B.grp + g0 + 32LL * q), ee = __ldg(B.grp + g0 + 32LL * q + 32);
+            const int m = min(32, nq - qb);
+            for (int l = 0; l < m; ++l) {
+                const int e0 = __shfl_sync(0xffffffffu, eb, l), e1 = __shfl_sync(0xffffffffu, ee, l);
+                if (lane == 0) {
+                    if (wrap) mbar_wait_sleep(&empty[s], (unsigned)((wrap - 1) & 1));
+                    unsigned char *slot = ring + s * SLOT;
+                    const long long a0 = e0 & ~7, a1 = ((long long)e1 + 7) & ~7LL;   // 16-byte bounds of both streams
+                    const unsigned cnt = (unsigned)(a1 - a0);
+                    const long long gq = g0 + 32LL * (qb + l);
+                    mbar_expect_tx(&full[s], cnt * 10u + 1024u + 144u);
+                    if (cnt) {
+                        bulk_g2s(slot, B.val + a0, cnt * 8u, &full[s]);
+                        bulk_g2s(slot + 8 * (size_t)R.cap, B.col + a0, cnt * 2u, &full[s]);
+                    }
+                    bulk_g2s(slot + 10 * (size_t)R.cap, B.len + gq * 32, 1024u, &full[s]);
+                    bulk_g2s(slot + 10 * (size_t)R.cap + 1024, B.grp + gq, 144u, &full[s]);
+                }
+                if (++s == R.ns) { s = 0; ++wrap; }
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const unsigned ltmask = (1u << lane) - 1u;
+    const long long row0 = (long long)blockIdx.x * RBS;
+    auto issue = [&](int j) {
+        double *dst = (j & 1) ? xs1 : xs0;
+        const long long w0 = info.z + (long long)j * B.W;
+        const long long len = min((long long)B.W, n - w0);
+        if (len & 1) dst[len - 1] = x[w0 + len - 1];
+        const unsigned bytes = (unsigned)((len & ~1LL) * 8);
+        mbar_expect_tx(&xfull[j & 1], bytes);
+        for (unsigned o = 0; o < bytes; o += 32768u)
+            bulk_g2s(reinterpret_cast<unsigned char *>(dst) + o, reinterpret_cast<const unsigned char *>(x + w0) + o,
+                     min(32768u, bytes - o), &xfull[j & 1]);
+    };
+    if (tid == 0) {
+        issue(0);
+        if (npass > 1) issue(1);
+    }
+    double acc[RPT][2];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = 0.0;
+    int s = 0;
+    unsigned ph = 0;
+    for (int j = 0; j < npass; ++j) {
+        mbar_wait_sleep(&xfull[j & 1], (unsigned)((j >> 1) & 1));
+        const double *xs = (j & 1) ? xs1 : xs0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            mbar_wait_sleep(&full[s], ph);
+            const unsigned char *slot = ring + s * SLOT;
+            const double *sval = reinterpret_cast<const double *>(slot);
+            const unsigned short *scol = reinterpret_cast<const unsigned short *>(slot + 8 * (size_t)R.cap);
+            const int *sgrp = reinterpret_cast<const int *>(slot + 10 * (size_t)R.cap + 1024);
+            const int e0 = sgrp[0] & ~7;
+            // groups w and w + 16 of the round: two independent chains, interleaved
+            const unsigned la = slot[10 * (size_t)R.cap + tid], lb = slot[10 * (size_t)R.cap + NC + tid];
+            int ba = sgrp[warp] - e0, bb = sgrp[warp + BAND_CW] - e0;
+            const unsigned maxl = __reduce_max_sync(0xffffffffu, max(la, lb));
+            double ra = acc[i][0], rb = acc[i][1];
+            // branch-free steps: a lane whose row has no k-th nonzero reads entry 0 / column 0
+            // (broadcast reads) and keeps its sum
+            for (unsigned k = 0; k < maxl; ++k) {
+                const bool pa = la > k, pb = lb > k;
+                const unsigned ma = __ballot_sync(0xffffffffu, pa), mb = __ballot_sync(0xffffffffu, pb);
+                const int ia = pa ? ba + __popc(ma & ltmask) : 0, ib = pb ? bb + __popc(mb & ltmask) : 0;
+                ba += __popc(ma);
+                bb += __popc(mb);
+                const double va = sval[ia], vb = sval[ib];
+                const unsigned ca = pa ? scol[ia] : 0u, cb = pb ? scol[ib] : 0u;
+                const double ta = __dadd_rn(ra, __dmul_rn(va, in.xf(xs[ca], 0)));       // csr_matvec order
+                const double tb = __dadd_rn(rb, __dmul_rn(vb, in.xf(xs[cb], 0)));
+                ra = pa ? ta : ra;
+                rb = pb ? tb : rb;
+            }
+            acc[i][0] = ra;
+            acc[i][1] = rb;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == R.ns) { s = 0; ph ^= 1; }
+        }
+        consumer_sync(NC);                          // every consumer warp is done with window buffer j & 1
+        if (tid == 0 && j + 2 < npass) issue(j + 2);
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const long long r = row0 + i * 1024 + h * NC + tid;
+            if (r < n) out[r] = acc[i][h];
+        }
+    }
+}
+
 }  // namespace kpl

@@ -157,7 +157,7 @@ def band_rows_per_thread(n):
 
 
 def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, window=None, rpt=None):
-    """(bd_val, bd_col, bd_len, bd_grp, bd_sb, rpt, W) or None -- the layout
+    """(bd_val, bd_col, bd_len, bd_grp, bd_sb, rpt, W, round_max) or None -- the layout
     include/kpl_b200.h documents under kpl_op.bd_*.  Index work only (values are
     permuted, never combined), done once per matrix with torch sorts on the
     device the CSR arrays live on."""
@@ -171,9 +171,6 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
         return None
     if mode == "auto" and (nnz < _BAND_MIN_ROW_NNZ * n or csr_lines_per_warp(col_idx_h) < _BAND_MIN_LINES):
         return None
-    W = int(window or os.environ.get("KPL_BAND_W", _BAND_W_MAX))
-    if W < 2 or W % 2 or W > _BAND_W_MAX:
-        raise ValueError(f"window SpMV: window length {W} (expected an even value in 2..{_BAND_W_MAX})")
     rpt = int(rpt or int(os.environ.get("KPL_BAND_RPT", 0)) or band_rows_per_thread(n))
     if not 1 <= rpt <= 8:
         raise ValueError("window SpMV: rows per thread must be in 1..8")
@@ -184,47 +181,84 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
     counts = (row_ptr[1:] - row_ptr[:-1]).long()
     rows = t.repeat_interleave(t.arange(n, device=dev), counts)
     sb = rows // RB
+    lrow = rows - sb * RB
     col = col_idx.long()
     big = t.iinfo(t.int64).max
     c_lo = t.full((nsb,), big, dtype=t.int64, device=dev).scatter_reduce_(0, sb, col, "amin", include_self=True)
     c_hi = t.full((nsb,), -1, dtype=t.int64, device=dev).scatter_reduce_(0, sb, col, "amax", include_self=True)
     c_lo = t.where(c_hi < 0, t.zeros_like(c_lo), c_lo) & ~1          # even: 16-byte bulk copies
     c_hi = t.clamp(c_hi, min=0)
-    npass = (c_hi - c_lo) // W + 1
-    pass0 = t.cumsum(npass, 0) - npass
-    NP = int(npass.sum())
+    rel = col - c_lo[sb]
+
+    def plan(W):
+        """Passes of window length W: (passes per super-block, first pass, total, pass of
+        every nonzero, (pass, row) lengths, most nonzeros in one round of 32 groups)."""
+        npass = (c_hi - c_lo) // W + 1
+        pass0 = t.cumsum(npass, 0) - npass
+        NP = int(npass.sum())
+        if NP * RB >= 2**31:
+            return None
+        p = pass0[sb] + rel // W
+        lens = t.bincount(p * RB + lrow, minlength=NP * RB)
+        round_max = int(lens.view(NP * rpt, 1024).sum(1).max())
+        return npass, pass0, NP, p, lens, round_max
+
+    explicit = window or os.environ.get("KPL_BAND_W")
+    if explicit:
+        W = int(explicit)
+        if W < 2 or W % 2 or W > _BAND_W_MAX:
+            raise ValueError(f"window SpMV: window length {W} (expected an even value in 2..{_BAND_W_MAX})")
+        pl = plan(W)
+    else:
+        # the widest window that leaves room for four ring slots of the matrix stream
+        # (csr_band_ring_spmv; config 5: 8192 columns, 0.270 ms/iteration against 0.287 with
+        # two slots at 10240); failing that, the plain-load kernel with the widest window
+        pl = None
+        for W in _BAND_RING_WINDOWS:
+            pl = plan(W)
+            if pl is not None and band_ring_slots(W, pl[5]) >= 4:
+                break
+        else:
+            W = _BAND_W_MAX
+            pl = plan(W)
+    if pl is None:
+        return None
+    npass, pass0, NP, p, lens, round_max = pl
     if mode == "auto" and NP * RB > _BAND_MAX_LEN_BYTES * 10.0 * nnz:
         return None                                                   # too wide a span for the window walk
-    if NP * RB >= 2**31 or NP * G + 1 >= 2**31:
-        return None
-    rel = col - c_lo[sb]
-    j = rel // W
-    p = pass0[sb] + j
-    bcol = rel - j * W
-    # (pass, local row) lengths; CSR order is (row, column) and j grows with the column,
-    # so a stable sort by the (pass, group, step, lane) key needs the entry's rank inside
-    # its (pass, row) segment
-    slot = p * RB + (rows - sb * RB)
-    lens = t.bincount(slot, minlength=NP * RB)
     if int(lens.max()) > 255:
         return None
+    bcol = rel - (rel // W) * W
+    # CSR order is (row, column) and the pass grows with the column, so the entry's rank
+    # inside its (pass, row) segment follows from a stable sort by (pass, row)
+    slot = p * RB + lrow
     order = t.argsort(slot, stable=True)                              # (pass, row, column)
     seg_start = t.cumsum(lens, 0) - lens
     k = t.empty_like(order)
     k[order] = t.arange(nnz, device=dev) - seg_start[slot[order]]
-    lrow = rows - sb * RB
-    key = ((p * G + lrow // 32) * 256 + k) * 32 + lrow % 32
+    key = ((p * G + lrow // 32) * 256 + k) * 32 + lrow % 32           # (pass, group, step, lane)
     perm = t.argsort(key)
     del key, k, order, seg_start, slot
-    pad = lambda a: t.cat([a, a.new_zeros(8)])
+    pad = lambda a: t.cat([a, a.new_zeros(8)])                        # bulk copies widen to 16-byte bounds
     bd_val = pad(values[perm])
     bd_col = pad(bcol[perm].to(t.int32).to(t.int16))                  # < 65536: uint16 bits
     bd_len = lens.to(t.uint8)
     gtot = lens.view(NP * G, 32).sum(1)
-    bd_grp = t.zeros(NP * G + 1, dtype=t.int32, device=dev)
-    bd_grp[1:] = t.cumsum(gtot, 0).to(t.int32)
+    bd_grp = t.full((NP * G + 8,), nnz, dtype=t.int32, device=dev)    # terminal entry + bulk-copy slack
+    bd_grp[0] = 0
+    bd_grp[1:NP * G + 1] = t.cumsum(gtot, 0).to(t.int32)
     bd_sb = t.stack([pass0, npass, c_lo, t.zeros_like(c_lo)], 1).to(t.int32).contiguous()
-    return bd_val, bd_col, bd_len, bd_grp, bd_sb, rpt, W
+    return bd_val, bd_col, bd_len, bd_grp, bd_sb, rpt, W, round_max
+
+
+_BAND_RING_WINDOWS = (8192, 7168, 6144, 5120, 4096)
+
+
+def band_ring_slots(W, round_max):
+    """Ring slots csr_band_ring_spmv gets next to two windows of W columns
+    (kpl_capi.cu:band_ring; < 2: the plain-load kernel runs instead)."""
+    cap = (round_max + 16 + 63) // 64 * 64
+    return min(4, (227 * 1024 - 16 * W - 128) // (10 * cap + 1024 + 144))
 
 
 # Column-sorted SpMV gathers (kpl_op.sp_*): meant for matrices whose CSR-order
@@ -415,9 +449,9 @@ def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk
             op.sp_col, op.sp_val, op.sp_dest = ptr(sc), ptr(sv), ptr(sd)
             op.sp_rows, op.sp_max = R, most
         if dm.band is not None:
-            bv, bc, bl, bg, bs, rpt, W = dm.band
+            bv, bc, bl, bg, bs, rpt, W, round_max = dm.band
             op.bd_val, op.bd_col, op.bd_len, op.bd_grp, op.bd_sb = ptr(bv), ptr(bc), ptr(bl), ptr(bg), ptr(bs)
-            op.bd_rpt, op.bd_w = rpt, W
+            op.bd_rpt, op.bd_w, op.bd_round_max = rpt, W, round_max
     op.zc = zc
     op.vx = vx
     op.chunk_blocks = chunk_blocks

@@ -13,7 +13,7 @@ from paper_1706_05988_b200.sparse import SparseMatrix
 
 def walk(layout, n, x):
     """What csr_band_spmv computes, one (super-block, pass, group, lane) at a time."""
-    val, col, ln, grp, sb, rpt, W = layout
+    val, col, ln, grp, sb, rpt, W, round_max = layout
     val, col = val.numpy(), col.numpy().view(np.uint16)
     ln, grp, sb = ln.numpy(), grp.numpy(), sb.numpy()
     RB, G = 1024 * rpt, 32 * rpt
@@ -36,6 +36,8 @@ def walk(layout, n, x):
                         acc[32 * g + lane] = acc[32 * g + lane] + val[e] * x[c]
                     base += len(lanes)
                 assert base == int(grp[p * G + g + 1])
+            for i in range(rpt):
+                assert int(grp[p * G + 32 * i + 32]) - int(grp[p * G + 32 * i]) <= round_max
         r0 = s * RB
         m = min(RB, n - r0)
         out[r0:r0 + m] = acc[:m]
@@ -59,7 +61,7 @@ def test_band_layout_walk_equals_csr_matvec(n, band, window, rpt):
     ref = O.spmv(O.as_oracle_operator(A), x)
     assert walk(lay, n, x).tobytes() == ref.tobytes()
     # every nonzero is stored exactly once
-    assert int(lay[3][-1]) == len(A.values)
+    assert int(lay[3][-8]) == len(A.values) and int(lay[3][-1]) == len(A.values)
     assert np.array_equal(np.sort(lay[0].numpy()[:-8]), np.sort(A.values))
 
 

@@ -60,10 +60,13 @@ def test_spmv_layouts_bitwise(monkeypatch, name, make):
     assert same_bits(outs["csr"], outs["band"])
 
 
-@pytest.mark.parametrize("window,rpt", [(2, 1), (64, 1), (1000, 2), (4096, 3), (14336, 8), (14336, 0)])
-def test_band_windows_and_block_heights_bitwise(monkeypatch, window, rpt):
-    """Many short passes, odd window tails (n odd), every super-block height."""
+@pytest.mark.parametrize("kernel", ["ring", "ldg"])
+@pytest.mark.parametrize("window,rpt", [(2, 1), (64, 1), (1000, 2), (4096, 3), (9216, 7), (14336, 8), (14336, 0)])
+def test_band_windows_and_block_heights_bitwise(monkeypatch, window, rpt, kernel):
+    """Many short passes, odd window tails (n odd), every super-block height; the
+    ring-fed kernel (bulk copies of the matrix stream) and the plain-load one."""
     monkeypatch.setenv("KPL_CSR_GATHER", "band")
+    monkeypatch.setenv("KPL_BAND_KERNEL", kernel)
     monkeypatch.setenv("KPL_BAND_W", str(window))
     monkeypatch.setenv("KPL_BAND_RPT", str(rpt))
     A = problems.banded_spd(9_001 if window <= 64 else 70_001, seed=window, band=700 if window <= 64 else 30_000)
@@ -80,7 +83,7 @@ def test_band_windows_and_block_heights_bitwise(monkeypatch, window, rpt):
 def test_auto_picks_the_window_layout_for_scattered_only(monkeypatch):
     monkeypatch.delenv("KPL_CSR_GATHER", raising=False)
     dev = D.require_cuda()
-    dm = D.device_matrix(fresh(problems.banded_spd(40_000, seed=0)), dev)
+    dm = D.device_matrix(fresh(problems.banded_spd(400_000, seed=0)), dev)
     assert dm.band is not None and dm.sorted is None
     dm = D.device_matrix(fresh(K.laplacian_2d(300, 300)), dev)
     assert dm.band is None and dm.sorted is None
