@@ -436,7 +436,13 @@ int launch(const kpl_op *op, const Layout &L, In in, Body body, const Ws &ws, co
     }
     if (ws.prod && phase != PH_NONE && Body::NQ > 0) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        blocked_final_kernel<<<1, 32, 0, st>>>(ws, cfg, phase, pred, row, Body::NQ);
+        // large even n: the chain fed from a shared-memory ring of bulk copies (same chain, ~8x faster)
+        if (ws.nprod >= (1 << 16) && ws.nprod % 2 == 0) {
+            cudaFuncSetAttribute(blocked_final_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BF_SMEM);
+            blocked_final_tma_kernel<<<1, 64, BF_SMEM, st>>>(ws, cfg, phase, pred, row, Body::NQ);
+        } else {
+            blocked_final_kernel<<<1, 32, 0, st>>>(ws, cfg, phase, pred, row, Body::NQ);
+        }
     }
     return cuda_check("sweep launch");
 }

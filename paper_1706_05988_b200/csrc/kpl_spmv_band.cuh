@@ -312,4 +312,90 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
     }
 }
 
+// ---------------------------------------------------------------------------
+// Reference-order fold (KPL_ORDER_BLOCKED8) for large n: blocked_final_kernel's
+// chain -- lane l of quantity q adds prod[q][l + 8 j] for j = 0, 1, ... -- fed
+// from shared memory.  One warp reading 4 GiB straight from HBM with 16 loads in
+// flight per thread is bound by memory latency (~0.7 s per fold at 512^3); here
+// a producer thread streams the product arrays through a ring of bulk copies
+// and the 32 chain threads only see shared-memory latency, so the fold runs at
+// the speed of its dependent fp64 adds.  Same chain, same bits.
+constexpr int BF_T = 2048;                         // elements per quantity per stage
+constexpr int BF_NS = 3;                           // stages
+constexpr int BF_QS = BF_T + 8;                    // quantity stride (64 bytes of padding: bank spread)
+constexpr size_t BF_SMEM = sizeof(double) * BF_NS * NQ * BF_QS + 16 * BF_NS;
+
+__global__ void __launch_bounds__(64) blocked_final_tma_kernel(Ws ws, Cfg cfg, int phase, int pred, long long row,
+                                                               int nq) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double lanes[NQ][8];
+    __shared__ double tails[NQ];
+    double *stage = reinterpret_cast<double *>(smem);
+    unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + sizeof(double) * BF_NS * NQ * BF_QS);
+    unsigned long long *empty = full + BF_NS;
+    if (!pred_ok(ws.head, pred, row)) return;
+    const long long n = ws.nprod, lim = n - n % 8;
+    const long long nst = (lim + BF_T - 1) / BF_T;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < BF_NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid >= 32) {
+        if (tid == 32) {
+            for (long long st = 0; st < nst; ++st) {
+                const int s = (int)(st % BF_NS);
+                if (st >= BF_NS) mbar_wait(&empty[s], (unsigned)(((st / BF_NS) - 1) & 1));
+                const unsigned m = (unsigned)min((long long)BF_T, lim - st * BF_T);
+                mbar_expect_tx(&full[s], (unsigned)nq * m * 8u);
+                for (int q = 0; q < nq; ++q)
+                    bulk_g2s(stage + ((size_t)s * NQ + q) * BF_QS, ws.prod + q * n + st * BF_T, m * 8u, &full[s]);
+            }
+        }
+        return;
+    }
+    const int q = tid >> 3, lane = tid & 7;
+    double a = 0.0;
+    for (long long st = 0; st < nst; ++st) {
+        const int s = (int)(st % BF_NS);
+        mbar_wait(&full[s], (unsigned)((st / BF_NS) & 1));
+        if (q < nq) {
+            const double *p = stage + ((size_t)s * NQ + q) * BF_QS + lane;
+            const int m = (int)min((long long)BF_T, lim - st * BF_T);
+            constexpr int U = 16;
+            int k = 0;
+            for (; k + 8 * U <= m; k += 8 * U) {
+                double t[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j) t[j] = p[k + 8 * j];
+#pragma unroll
+                for (int j = 0; j < U; ++j) a = __dadd_rn(a, t[j]);
+            }
+            for (; k < m; k += 8) a = __dadd_rn(a, p[k]);
+        }
+        __syncwarp();
+        if (tid == 0) mbar_arrive(&empty[s]);
+    }
+    if (q < nq) {
+        lanes[q][lane] = a;
+        if (lane == 0) {
+            double t = 0.0;
+            for (long long j = lim; j < n; ++j) t = __dadd_rn(t, __ldcg(ws.prod + q * n + j));
+            tails[q] = t;
+        }
+    }
+    __syncwarp();
+    if (tid == 0) {
+        double v[NQ] = {0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i < nq; ++i) {
+            const double *l = lanes[i];
+            v[i] = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(l[0], l[1]), __dadd_rn(l[2], l[3])),
+                                       __dadd_rn(__dadd_rn(l[4], l[5]), __dadd_rn(l[6], l[7]))),
+                             tails[i]);
+        }
+        finalize(ws, cfg, phase, v);
+    }
+}
+
 }  // namespace kpl

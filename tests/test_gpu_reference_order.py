@@ -180,3 +180,22 @@ def test_reference_order_refused_for_partitioned_solves():
     with pytest.raises(KplError):
         solve_distributed(A, None, [np.ones(256), np.ones(256)], None,
                           K.SolverConfig(method="pcg_sh", shift=1.0, max_iters=5), comm=LocalComm(2))
+
+
+@pytest.mark.parametrize("shape,m,extra", [((512, 256), "pcg_sh", {"shift": 1.5}), ((300, 301), "pcg_rr", {}),
+                                            ((64, 48, 40), "pcg_sh", {"shift": 2.0}), ((257, 255), "cg", {})])
+def test_streamed_fold_equals_the_oracle_chain(shape, m, extra):
+    """n >= 65536 and even: the reference-order fold runs from a shared-memory ring
+    of bulk copies (blocked_final_tma_kernel); odd n keeps the plain-load fold.  Both
+    must reproduce the oracle's blocked_dot run (pinned to the reference) bit for bit."""
+    from oracle import kpl_oracle as O
+    A = K.Stencil3D(*shape) if len(shape) == 3 else K.Stencil2D(*shape)
+    oA = O.as_oracle_operator(A)
+    b = O.spmv(oA, np.random.default_rng(4).standard_normal(A.n))
+    kw = dict(method=m, max_iters=25, rtol=0.0, **extra)
+    res = K.solve(A, None, b, None, K.SolverConfig(**kw))
+    ref = O.solve(oA, None, b, None, O.Config(**kw))
+    got = np.array([[r.alpha, r.beta, r.gamma, r.delta, r.rnorm_recursive] for r in res.history])
+    want = np.ascontiguousarray(ref.history[:, 1:6])
+    assert got.tobytes() == want.tobytes(), first_diff(got, want)
+    assert np.asarray(res.x).tobytes() == ref.x.tobytes()
