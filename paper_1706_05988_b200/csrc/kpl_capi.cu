@@ -969,6 +969,17 @@ int do_sweep(const Ctx &c, int kind, long long row) {
         in.p0 = v->p; in.p1 = v->p1; in.u = u; in.p = v->p; in.beta = 0.0;
         BodyCgP bp;
         bp.p0 = v->p; bp.p1 = v->p1; bp.s = v->s; bp.pout = v->p1;
+        {
+            // window SpMV: materialise p_new first so the SpMV gathers one plain vector from shared memory
+            const InVec<KPL_PC_IDENTITY> pn = in_vec<KPL_PC_IDENTITY>(op, v->p, v->p1, SEL_ITER1);
+            if (op->kind == KPL_OP_CSR && band_ok(op, pn)) {
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                const unsigned grid = (unsigned)std::min<long long>(cdiv(op->n, 256), 8LL * kSMs);
+                launch_pdl(cg_p_materialise_kernel, grid, 256, 0, c.st, (long long)op->n, in, v->p, v->p1, c.ws, pred,
+                           row);
+                return launch(op, L, in, bp, c.ws, c.cfg, phase, pred, row, c.st, pn);
+            }
+        }
         return launch(op, L, in, bp, c.ws, c.cfg, phase, pred, row, c.st);
     }
     case KPL_SW_CG_X: {                  // x, r, u updates + next head (:290-292, :258-259)

@@ -398,4 +398,22 @@ __global__ void __launch_bounds__(64) blocked_final_tma_kernel(Ws ws, Cfg cfg, i
     }
 }
 
+// Classic CG with the window SpMV: p_new = axpy(beta, p_old, u) (solvers.py:269) written
+// out first, so the SpMV reads a plain vector (the CSR-order kernels evaluate it per
+// gathered column instead: two gathers per nonzero).  Same expression as InCgP::raw,
+// and csr_chunk_sweep's BodyCgP stores the same values again.
+__global__ void __launch_bounds__(256) cg_p_materialise_kernel(long long n, InCgP in, double *p0, double *p1, Ws ws,
+                                                               int pred, long long row) {
+    pdl_wait();
+    pdl_launch_dependents();
+    if (!pred_ok(ws.head, pred, row)) return;
+    in.setup(ws);
+    double *pout = const_cast<double *>(pick(ws.head, SEL_ITER1, p0, p1));
+    for (long long k = blockIdx.x * 256LL + threadIdx.x; k < n; k += 256LL * gridDim.x) {
+        double o[1];
+        in.template raw<1>(in.base(), k, o);
+        pout[k] = o[0];
+    }
+}
+
 }  // namespace kpl
