@@ -114,32 +114,35 @@ typedef struct kpl_op {
     int32_t sp_max;
     /* CSR, optional shared-memory-window layout of the SpMV for scattered
        banded matrices (NULL = not used; takes precedence over sp_*).  Rows are
-       grouped in super-blocks of 1024*bd_rpt rows, one CTA each.  Super-block s
+       grouped in super-blocks of bd_rows rows, one CTA each.  Super-block s
        walks its column span in bd_sb[4s+1] windows of bd_w columns starting at
        column bd_sb[4s+2] (even); window j of super-block s is "pass"
-       p = bd_sb[4s] + j, and the CTA holds the window's slice of the input
-       vector in shared memory (bulk copies, double-buffered), so the gathers
-       are shared-memory loads.  Inside a pass the rows come in groups of 32
-       (group g = rows 32g..32g+31 of the super-block); bd_len[p*RB + t] is the
-       number of nonzeros of local row t inside the window (<= 255) and the
-       group's nonzeros start at bd_grp[p*RB/32 + g] (one terminal entry at the
-       end), stored in jagged-diagonal order: step k of every row that has one,
-       in lane order.  bd_val / bd_col hold the values and the columns relative
-       to the window start (uint16).  Lane l sums row l's products left to
-       right across the passes, i.e. in ascending column order from +0.0: the
-       csr_matvec order (_kernels.py:44-52), bit for bit.                      */
+       p = bd_sb[4s] + j.  The CTA keeps the window's slice of the input vector
+       in shared memory (bulk copies, double-buffered), so the gathers are
+       shared-memory loads, and the running sum of every row of the super-block
+       in shared memory as well.
+       A pass has RBP = 1024*ceil(bd_rows/1024) slots; slot t of pass p works on
+       local row bd_row[p*RBP + t], which has bd_len[p*RBP + t] (<= 255) nonzeros
+       inside the window.  Slots are ordered so that the 32 slots of a group
+       hold rows of (nearly) equal length, longest first, and the groups of a
+       pass are dealt to its ceil(bd_rows/1024) rounds of 32 groups in turn.
+       Group g (32 slots 32g..32g+31, counted over all passes) stores L full
+       steps of 32 entries from bd_grp[g] on (L = its longest row; entry 32k+l
+       is the k-th nonzero of slot l's row, zero-filled past the row's end):
+       bd_val / bd_col hold the values and the columns relative to the window
+       start (uint16).  A lane adds its row's products to the row's running sum
+       left to right, pass after pass, i.e. in ascending column order from
+       +0.0: the csr_matvec order (_kernels.py:44-52), bit for bit.
+       bd_round_max = most entries in one round.  Padding: 64 spare entries
+       after bd_val / bd_col, 8 spare ints after bd_grp (bulk copies).        */
     const double   *bd_val;
     const uint16_t *bd_col;
+    const uint16_t *bd_row;
     const uint8_t  *bd_len;
     const int32_t  *bd_grp;
     const int32_t  *bd_sb;
-    int32_t bd_rpt;          /* 1..8: rows per super-block / 1024                 */
+    int32_t bd_rows;         /* rows per super-block (multiple of 32, <= 4608)    */
     int32_t bd_w;            /* window length in columns (even, <= 65536)         */
-    /* most nonzeros in one round (32 consecutive groups of one pass); > 0
-       selects the ring-fed kernel, which streams bd_val/bd_col/bd_len/bd_grp
-       through shared memory with bulk copies when at least two ring slots of
-       this size fit next to the two windows.  The arrays then need 8 spare
-       entries (bd_val, bd_col) / 4 spare ints (bd_grp) of padding at the end. */
     int32_t bd_round_max;
     int32_t _reserved2;
 } kpl_op;

@@ -53,6 +53,16 @@ long long align256(long long v) { return (v + 255) & ~255LL; }
 
 constexpr int kSMs = 148;
 
+// ring slots of the window SpMV that fit next to the running sums and the two windows
+// (device.py:band_ring_slots computes the same)
+BandRing band_ring(const kpl_op *op) {
+    BandRing r{0, 0};
+    r.cap = (op->bd_round_max + 63) / 64 * 64;
+    const long long room = 227LL * 1024 - 8LL * op->bd_rows - 16LL * op->bd_w - 128;
+    r.ns = (int)std::max<long long>(0, std::min<long long>(4, room / (long long)r.slot()));
+    return r;
+}
+
 int make_layout(const kpl_op *op, Layout &L) {
     if (!op) return fail(KPL_EINVAL, "null operator");
     std::memset(&L, 0, sizeof(L));
@@ -94,9 +104,9 @@ int make_layout(const kpl_op *op, Layout &L) {
         if (op->sp_col && (!op->sp_val || !op->sp_dest || op->sp_rows < 1 || op->sp_max < 1 ||
                            op->sp_max > 65535 || 8LL * op->sp_max > 227 * 1024))
             return fail(KPL_EINVAL, "bad column-sorted SpMV layout");
-        if (op->bd_val && (!op->bd_col || !op->bd_len || !op->bd_grp || !op->bd_sb || op->bd_rpt < 1 ||
-                           op->bd_rpt > 8 || op->bd_w < 2 || (op->bd_w & 1) || op->bd_w > 65536 ||
-                           16LL * op->bd_w + 64 > 227 * 1024))
+        if (op->bd_val && (!op->bd_col || !op->bd_row || !op->bd_len || !op->bd_grp || !op->bd_sb ||
+                           op->bd_rows < 32 || op->bd_rows % 32 || op->bd_rows > 4608 || op->bd_w < 2 ||
+                           (op->bd_w & 1) || op->bd_w > 65536 || op->bd_round_max < 0 || band_ring(op).ns < 2))
             return fail(KPL_EINVAL, "bad window SpMV layout");
         L.vx = 1; L.wx = NWARP; L.wy = 1; L.zc = cb;
         L.T = cb;
@@ -287,11 +297,10 @@ void launch_sorted(const kpl_op *op, const CGeo &g, const SIn &in, double *out, 
     }
 }
 
-// Shared-memory-window SpMV (kpl_op.bd_*): one CTA per super-block of 1024*bd_rpt
-// rows, 16*bd_w bytes of dynamic shared memory (two input windows).  Taken for
-// plain vector inputs whose storage allows 16-byte bulk copies; anything else
-// (classic CG's p = beta*p + u evaluated on the fly, a Jacobi diagonal gathered
-// per column) keeps the CSR-order kernels.
+// Shared-memory-window SpMV (kpl_op.bd_*): one CTA per super-block of bd_rows rows.
+// Taken for plain vector inputs whose storage allows 16-byte bulk copies; anything
+// else (a Jacobi diagonal gathered per column, multi-GPU row blocks) keeps the
+// CSR-order kernels.
 template <class SIn> struct band_capable : std::false_type {};
 template <> struct band_capable<InVec<KPL_PC_IDENTITY, 0>> : std::true_type {};
 
@@ -304,54 +313,18 @@ bool band_ok(const kpl_op *op, const SIn &in) {
     }
 }
 
-// ring slots that fit next to the two windows (0: the plain-load kernel)
-BandRing band_ring(const kpl_op *op) {
-    const char *e = std::getenv("KPL_BAND_KERNEL");       // read per launch: the tests switch it
-    const bool off = e && !std::strcmp(e, "ldg");
-    BandRing r{0, 0};
-    if (off || op->bd_round_max <= 0) return r;
-    r.cap = (op->bd_round_max + 16 + 63) / 64 * 64;
-    const long long room = 227LL * 1024 - 16LL * op->bd_w - 128;
-    r.ns = (int)std::min<long long>(4, room / (long long)r.slot());
-    if (r.ns < 2) r.ns = 0;
-    return r;
-}
-
-template <class SIn, int RPT>
-void launch_band_rpt(const kpl_op *op, const BandGeo &bg, const SIn &in, double *out, const Ws &ws, int pred,
-                     long long row, cudaStream_t st) {
-    const BandRing ring = band_ring(op);
-    if (ring.ns) {
-        auto kern = csr_band_ring_spmv<SIn, RPT>;
-        const size_t smem = ring.bytes(op->bd_w);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const unsigned grid = (unsigned)cdiv(op->n, 1024LL * RPT);
-        launch_pdl(kern, grid, BAND_CW * 32 + 32, smem, st, (long long)op->n, bg, ring, in, out, ws, pred, row);
-        return;
-    }
-    auto kern = csr_band_spmv<SIn, RPT, 2>;
-    const size_t smem = 16 * (size_t)op->bd_w + 64;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const unsigned grid = (unsigned)cdiv(op->n, 1024LL * RPT);
-    launch_pdl(kern, grid, 1024, smem, st, (long long)op->n, bg, in, out, ws, pred, row);
-}
-
 template <class SIn>
 void launch_band(const kpl_op *op, const SIn &in, double *out, const Ws &ws, int pred, long long row,
                  cudaStream_t st) {
     if constexpr (band_capable<SIn>::value) {
-        const BandGeo bg{op->bd_val, op->bd_col, op->bd_len, op->bd_grp, reinterpret_cast<const int4 *>(op->bd_sb),
-                         op->bd_w};
-        switch (op->bd_rpt) {
-        case 1: launch_band_rpt<SIn, 1>(op, bg, in, out, ws, pred, row, st); break;
-        case 2: launch_band_rpt<SIn, 2>(op, bg, in, out, ws, pred, row, st); break;
-        case 3: launch_band_rpt<SIn, 3>(op, bg, in, out, ws, pred, row, st); break;
-        case 4: launch_band_rpt<SIn, 4>(op, bg, in, out, ws, pred, row, st); break;
-        case 5: launch_band_rpt<SIn, 5>(op, bg, in, out, ws, pred, row, st); break;
-        case 6: launch_band_rpt<SIn, 6>(op, bg, in, out, ws, pred, row, st); break;
-        case 7: launch_band_rpt<SIn, 7>(op, bg, in, out, ws, pred, row, st); break;
-        default: launch_band_rpt<SIn, 8>(op, bg, in, out, ws, pred, row, st); break;
-        }
+        const BandGeo bg{op->bd_val, op->bd_col, op->bd_row, op->bd_len, op->bd_grp,
+                         reinterpret_cast<const int4 *>(op->bd_sb), op->bd_w, op->bd_rows};
+        const BandRing ring = band_ring(op);
+        auto kern = csr_band_ring_spmv<SIn>;
+        const size_t smem = ring.bytes(op->bd_rows, op->bd_w);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const unsigned grid = (unsigned)cdiv(op->n, (long long)op->bd_rows);
+        launch_pdl(kern, grid, BAND_CW * 32 + 32, smem, st, (long long)op->n, bg, ring, in, out, ws, pred, row);
     }
 }
 

@@ -4,24 +4,44 @@
 // A CSR-order warp gather from global memory touches ~31 distinct cache lines
 // and the L1 tag stage takes one line per cycle: config 5's 45.4 M gathers cost
 // 170 us on their own (tools/gather_bench.cu), which bounds csr_spmv_pipe at
-// ~237 us.  Shared memory has no tag stage.  Here one CTA owns a super-block of
-// RPT*1024 rows and walks the super-block's column span in windows of W columns;
+// ~231 us.  Shared memory has no tag stage.  Here one CTA owns a super-block of
+// bd_rows rows and walks the super-block's column span in windows of W columns;
 // each window's slice of the input vector is staged in shared memory by bulk
 // copies (cp.async.bulk, double-buffered: window j+2 lands while window j+1 is
 // used), and the gathers become shared-memory loads.
 //
-// Order of the sums: thread t keeps the accumulators of rows t, t+1024, ... in
-// registers across the passes.  The windows are visited in ascending column
-// order and a row's nonzeros inside a window keep their CSR order, so every row
-// is summed left to right from +0.0: csr_matvec (_kernels.py:44-52) bit for bit.
+// Order of the sums: the running sum of every row of the super-block lives in
+// shared memory.  The windows are visited in ascending column order and a row's
+// nonzeros inside a window keep their CSR order, so every row is summed left to
+// right from +0.0: csr_matvec (_kernels.py:44-52) bit for bit.
 //
-// Stream layout (built once per matrix, device.py:band_layout): inside a
-// (pass, 32-row group) the nonzeros are stored in jagged-diagonal order -- step
-// k of every row that has a k-th nonzero in the window, in lane order -- so the
-// lanes that take step k read consecutive entries (coalesced), each its own
-// row's next nonzero; the position comes from a ballot over the row lengths.
-// 10 bytes per nonzero (fp64 value + uint16 window-relative column) + 1 byte
-// per (row, pass) against CSR's 12.
+// Lane use: inside a window a row holds only ~2 of its ~23 nonzeros, with a wide
+// spread (0..6), so a warp that takes 32 consecutive rows idles most lanes most
+// steps (measured: 41 % lane use, the kernel bound by instruction issue).  The
+// layout (device.py:band_layout) therefore sorts the rows of a pass by their
+// length inside the window: a group's 32 slots hold rows of (nearly) equal
+// length and are stored as L full steps of 32 entries -- lane l's k-th nonzero at
+// entry 32 k + l, no index arithmetic beyond that, ~100 % lane use.  The price is
+// the slot -> row indirection (2 bytes per row and pass) and the running sums in
+// shared memory instead of registers.
+//
+// The matrix stream never touches the LSU's global path: with ~220 KB of the
+// SM's 256 KB carved out as shared memory almost no L1 is left, and plain loads
+// run out of L1 miss slots long before the DRAM rate (measured on the first
+// form of this kernel: 17 of 32 warps on the long scoreboard, DRAM at 40 %).  A
+// producer warp moves the stream with cp.async.bulk into a ring of shared-memory
+// slots, one slot per "round" (32 groups: their entries, slot rows, slot lengths
+// and group offsets -- five contiguous slices of the bd_* arrays):
+//
+//   smem = | sums[rows] | window 0 [W] | window 1 [W] | ring[ns] | barriers |
+//   slot = | val[cap] | col[cap] | row[1024] | len[1024] | grp[36] |     cap % 64 == 0
+//   barriers: xfull[2] (input windows), full[ns] (1 arrival + bytes), empty[ns] (16 arrivals)
+//
+//   warp 16 (producer)                           warps 0..15 (consumers)
+//   ------------------------------------        ---------------------------------------------------------
+//   round boundaries 32 at a time (one per       per pass: wait the window; per round: wait full[slot],
+//   lane); per round: wait empty[slot],          walk groups w and w + 16 (two independent chains),
+//   expect_tx, 5 bulk copies                     arrive on empty[slot]; bar.sync among consumers, window j+2
 #pragma once
 #include "kpl_spmv_tma.cuh"
 
@@ -30,137 +50,19 @@ namespace kpl {
 struct BandGeo {
     const double *val;
     const unsigned short *col;
+    const unsigned short *rowi;
     const unsigned char *len;
     const int *grp;
     const int4 *sb;           // {first pass, passes, first column (even), -}
-    int W;
+    int W, rows;
 };
 
-template <class In, int RPT, int UN>
-__global__ void __launch_bounds__(1024, 1)
-csr_band_spmv(long long n, BandGeo B, In in, double *__restrict__ out, Ws ws, int pred, long long row) {
-    constexpr int RBS = RPT * 1024, G = RBS / 32;
-    extern __shared__ __align__(128) unsigned char smem[];
-    double *xs0 = reinterpret_cast<double *>(smem);
-    double *xs1 = xs0 + B.W;
-    unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + 16 * (size_t)B.W);
-    pdl_wait();
-    pdl_launch_dependents();
-    if (ws.head && !pred_ok(ws.head, pred, row)) return;
-    if (ws.head) in.setup(ws);
-    const double *x = in.base();
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const unsigned ltmask = (1u << lane) - 1u;
-    const int4 info = __ldg(B.sb + blockIdx.x);
-    const int pass0 = info.x, npass = info.y;
-    const long long row0 = (long long)blockIdx.x * RBS;
-    if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // window j -> buffer j & 1; an odd tail element goes in with a plain store
-    // (made visible by the release of the expect_tx arrive that follows it)
-    auto issue = [&](int j) {
-        double *dst = (j & 1) ? xs1 : xs0;
-        const long long w0 = info.z + (long long)j * B.W;
-        const long long len = min((long long)B.W, n - w0);
-        if (len & 1) dst[len - 1] = x[w0 + len - 1];
-        const unsigned bytes = (unsigned)((len & ~1LL) * 8);
-        mbar_expect_tx(&full[j & 1], bytes);
-        for (unsigned o = 0; o < bytes; o += 32768u)
-            bulk_g2s(reinterpret_cast<unsigned char *>(dst) + o, reinterpret_cast<const unsigned char *>(x + w0) + o,
-                     min(32768u, bytes - o), &full[j & 1]);
-    };
-    if (tid == 0) {
-        issue(0);
-        if (npass > 1) issue(1);
-    }
-    double acc[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[i] = 0.0;
-    for (int j = 0; j < npass; ++j) {
-        const long long p = pass0 + j;
-        unsigned L[RPT];
-        int gb[RPT];
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            L[i] = __ldg(B.len + p * RBS + i * 1024 + tid);
-            gb[i] = __ldg(B.grp + p * G + i * 32 + warp);
-        }
-        mbar_wait(&full[j & 1], (unsigned)((j >> 1) & 1));
-        const double *xs = (j & 1) ? xs1 : xs0;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            const unsigned len = L[i];
-            const unsigned maxl = __reduce_max_sync(0xffffffffu, len);
-            int base = gb[i];
-            for (unsigned k = 0; k < maxl; k += UN) {
-                double v[UN];
-                int c[UN];
-                bool act[UN];
-#pragma unroll
-                for (int u = 0; u < UN; ++u) {
-                    act[u] = len > k + u;
-                    const unsigned m = __ballot_sync(0xffffffffu, act[u]);
-                    const int idx = base + __popc(m & ltmask);
-                    base += __popc(m);
-                    v[u] = 0.0;
-                    c[u] = 0;
-                    if (act[u]) {
-                        v[u] = __ldcs(B.val + idx);
-                        c[u] = __ldcs(B.col + idx);
-                    }
-                }
-                double xv[UN];
-#pragma unroll
-                for (int u = 0; u < UN; ++u) xv[u] = xs[c[u]];
-#pragma unroll
-                for (int u = 0; u < UN; ++u)
-                    if (act[u]) acc[i] = __dadd_rn(acc[i], __dmul_rn(v[u], in.xf(xv[u], 0)));   // csr_matvec order
-            }
-        }
-        __syncthreads();                        // every warp is done with buffer j & 1
-        if (tid == 0 && j + 2 < npass) issue(j + 2);
-    }
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-        const long long r = row0 + i * 1024 + tid;
-        if (r < n) out[r] = acc[i];
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Ring-fed form.  With ~224 KB of the SM's 256 KB carved out as shared memory
-// almost no L1 is left, and the value/column stream of csr_band_spmv (plain
-// loads) runs out of L1 miss slots long before it reaches the DRAM rate: the
-// kernel is latency-bound (ncu: 17 of 32 warps on the long scoreboard, DRAM at
-// 40 %).  Here the stream never touches the LSU's global path: a producer warp
-// moves it with cp.async.bulk into a ring of shared-memory slots, one slot per
-// "round" (32 consecutive groups of a pass: their values, columns, row lengths
-// and group offsets -- four contiguous slices of the bd_* arrays), and the 16
-// consumer warps (two groups of a round each) read values, columns and the
-// input window from shared memory only.  Same walk, same sums: bit-identical
-// to csr_band_spmv.
-//
-//   slot = | val[cap] | col[cap] | len[1024] | grp[36] |     cap % 64 == 0
-//   barriers: xfull[2] (input windows), full[ns] (1 arrival + bytes), empty[ns] (16 arrivals)
-//
-//   warp 16 (producer)                           warps 0..15 (consumers), thread t: rows t + 512 h + 1024 i
-//   ------------------------------------        ---------------------------------------------------------
-//   round boundaries 32 at a time (one per       per pass: wait the window; per round: wait full[slot],
-//   lane); per round: wait empty[slot],          walk groups w and w + 16 (two independent chains),
-//   expect_tx, 4 bulk copies                     arrive on empty[slot]; bar.sync among consumers, window j+2
-//
-// (A CTA cannot exceed 1024 threads.  Measured alternatives on config 5: all 32
-// warps consuming with the producer role rotating among them -- every round then
-// waits for the slowest warp, 0.51 ms/iteration -- or with warp 0 feeding the
-// ring between its own groups without blocking -- fills lag, 0.37; this form: 0.27.)
 struct BandRing {
     int cap, ns;
-    __host__ __device__ size_t slot() const { return 10 * (size_t)cap + 1024 + 144; }
-    __host__ __device__ size_t bytes(int W) const { return 16 * (size_t)W + ns * slot() + 8 * (2 + 2 * (size_t)ns); }
+    __host__ __device__ size_t slot() const { return 10 * (size_t)cap + 3 * 1024 + 144; }
+    __host__ __device__ size_t bytes(int rows, int W) const {
+        return 8 * (size_t)rows + 16 * (size_t)W + ns * slot() + 8 * (2 + 2 * (size_t)ns);
+    }
 };
 
 // try_wait with a suspend-time hint: a waiting warp sleeps instead of spinning on the barrier word
@@ -178,15 +80,17 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long *b, unsigned 
 
 constexpr int BAND_CW = 16;                        // consumer warps
 
-template <class In, int RPT>
+template <class In>
 __global__ void __launch_bounds__(BAND_CW * 32 + 32, 1)
 csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict__ out, Ws ws, int pred,
                    long long row) {
-    constexpr int RBS = RPT * 1024, G = RBS / 32, NC = BAND_CW * 32;
+    constexpr int NC = BAND_CW * 32;
     extern __shared__ __align__(128) unsigned char smem[];
-    double *xs0 = reinterpret_cast<double *>(smem);
+    const int RB = B.rows, RP = (RB + 1023) >> 10;     // rows, rounds per pass
+    double *sums = reinterpret_cast<double *>(smem);
+    double *xs0 = sums + RB;
     double *xs1 = xs0 + B.W;
-    unsigned char *ring = smem + 16 * (size_t)B.W;
+    unsigned char *ring = reinterpret_cast<unsigned char *>(xs1 + B.W);
     const size_t SLOT = R.slot();
     unsigned long long *xfull = reinterpret_cast<unsigned long long *>(ring + R.ns * SLOT);
     unsigned long long *full = xfull + 2;
@@ -205,12 +109,13 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
         for (int s = 0; s < R.ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], BAND_CW); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int t = tid; t < RB; t += NC + 32) sums[t] = 0.0;      // +0.0: the reference's accumulator
     __syncthreads();
 
     if (warp == BAND_CW) {
         // ------------------------------------------------------------ producer
-        const int nq = npass * RPT;                    // rounds of this super-block
-        const long long g0 = (long long)pass0 * G;     // its first group
+        const int nq = npass * RP;                     // rounds of this super-block
+        const long long g0 = (long long)pass0 * RP * 32;   // its first group
         int s = 0, wrap = 0;
         for (int qb = 0; qb < nq; qb += 32) {
             // round boundaries of the next 32 rounds, one per lane
@@ -222,16 +127,16 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
                 if (lane == 0) {
                     if (wrap) mbar_wait_sleep(&empty[s], (unsigned)((wrap - 1) & 1));
                     unsigned char *slot = ring + s * SLOT;
-                    const long long a0 = e0 & ~7, a1 = ((long long)e1 + 7) & ~7LL;   // 16-byte bounds of both streams
-                    const unsigned cnt = (unsigned)(a1 - a0);
+                    const unsigned cnt = (unsigned)(e1 - e0);      // a multiple of 32 entries
                     const long long gq = g0 + 32LL * (qb + l);
-                    mbar_expect_tx(&full[s], cnt * 10u + 1024u + 144u);
+                    mbar_expect_tx(&full[s], cnt * 10u + 3u * 1024u + 144u);
                     if (cnt) {
-                        bulk_g2s(slot, B.val + a0, cnt * 8u, &full[s]);
-                        bulk_g2s(slot + 8 * (size_t)R.cap, B.col + a0, cnt * 2u, &full[s]);
+                        bulk_g2s(slot, B.val + e0, cnt * 8u, &full[s]);
+                        bulk_g2s(slot + 8 * (size_t)R.cap, B.col + e0, cnt * 2u, &full[s]);
                     }
-                    bulk_g2s(slot + 10 * (size_t)R.cap, B.len + gq * 32, 1024u, &full[s]);
-                    bulk_g2s(slot + 10 * (size_t)R.cap + 1024, B.grp + gq, 144u, &full[s]);
+                    bulk_g2s(slot + 10 * (size_t)R.cap, B.rowi + gq * 32, 2048u, &full[s]);
+                    bulk_g2s(slot + 10 * (size_t)R.cap + 2048, B.len + gq * 32, 1024u, &full[s]);
+                    bulk_g2s(slot + 10 * (size_t)R.cap + 3072, B.grp + gq, 144u, &full[s]);
                 }
                 if (++s == R.ns) { s = 0; ++wrap; }
             }
@@ -240,8 +145,8 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
     }
 
     // ---------------------------------------------------------------- consumers
-    const unsigned ltmask = (1u << lane) - 1u;
-    const long long row0 = (long long)blockIdx.x * RBS;
+    // window j -> buffer j & 1; an odd tail element goes in with a plain store
+    // (made visible by the release of the expect_tx arrive that follows it)
     auto issue = [&](int j) {
         double *dst = (j & 1) ? xs1 : xs0;
         const long long w0 = info.z + (long long)j * B.W;
@@ -257,44 +162,47 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
         issue(0);
         if (npass > 1) issue(1);
     }
-    double acc[RPT][2];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = 0.0;
     int s = 0;
     unsigned ph = 0;
     for (int j = 0; j < npass; ++j) {
         mbar_wait_sleep(&xfull[j & 1], (unsigned)((j >> 1) & 1));
         const double *xs = (j & 1) ? xs1 : xs0;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
+        for (int i = 0; i < RP; ++i) {
             mbar_wait_sleep(&full[s], ph);
             const unsigned char *slot = ring + s * SLOT;
             const double *sval = reinterpret_cast<const double *>(slot);
             const unsigned short *scol = reinterpret_cast<const unsigned short *>(slot + 8 * (size_t)R.cap);
-            const int *sgrp = reinterpret_cast<const int *>(slot + 10 * (size_t)R.cap + 1024);
-            const int e0 = sgrp[0] & ~7;
-            // groups w and w + 16 of the round: two independent chains, interleaved
-            const unsigned la = slot[10 * (size_t)R.cap + tid], lb = slot[10 * (size_t)R.cap + NC + tid];
-            int ba = sgrp[warp] - e0, bb = sgrp[warp + BAND_CW] - e0;
-            const unsigned maxl = __reduce_max_sync(0xffffffffu, max(la, lb));
-            double ra = acc[i][0], rb = acc[i][1];
-            // branch-free steps: a lane whose row has no k-th nonzero reads entry 0 / column 0
-            // (broadcast reads) and keeps its sum
-            for (unsigned k = 0; k < maxl; ++k) {
-                const bool pa = la > k, pb = lb > k;
-                const unsigned ma = __ballot_sync(0xffffffffu, pa), mb = __ballot_sync(0xffffffffu, pb);
-                const int ia = pa ? ba + __popc(ma & ltmask) : 0, ib = pb ? bb + __popc(mb & ltmask) : 0;
-                ba += __popc(ma);
-                bb += __popc(mb);
-                const double va = sval[ia], vb = sval[ib];
-                const unsigned ca = pa ? scol[ia] : 0u, cb = pb ? scol[ib] : 0u;
-                const double ta = __dadd_rn(ra, __dmul_rn(va, in.xf(xs[ca], 0)));       // csr_matvec order
-                const double tb = __dadd_rn(rb, __dmul_rn(vb, in.xf(xs[cb], 0)));
-                ra = pa ? ta : ra;
-                rb = pb ? tb : rb;
+            const unsigned short *srow = reinterpret_cast<const unsigned short *>(slot + 10 * (size_t)R.cap);
+            const unsigned char *slen = slot + 10 * (size_t)R.cap + 2048;
+            const int *sgrp = reinterpret_cast<const int *>(slot + 10 * (size_t)R.cap + 3072);
+            const int e0 = sgrp[0];
+            // groups w and w + 16 of the round: two independent chains, interleaved.  Lane 0 holds
+            // the group's longest row, lane 31 its shortest.
+            const unsigned la = slen[tid], lb = slen[NC + tid];
+            const unsigned ra_i = srow[tid], rb_i = srow[NC + tid];
+            const double *pa = sval + (sgrp[warp] - e0) + lane, *pb = sval + (sgrp[warp + BAND_CW] - e0) + lane;
+            const unsigned short *ca = scol + (sgrp[warp] - e0) + lane, *cb = scol + (sgrp[warp + BAND_CW] - e0) + lane;
+            const unsigned maxa = __shfl_sync(0xffffffffu, la, 0), maxb = __shfl_sync(0xffffffffu, lb, 0);
+            const unsigned mina = __shfl_sync(0xffffffffu, la, 31), minb = __shfl_sync(0xffffffffu, lb, 31);
+            double ra = la ? sums[ra_i] : 0.0, rb = lb ? sums[rb_i] : 0.0;
+            const unsigned both = min(mina, minb);
+            unsigned k = 0;
+            for (; k < both; ++k) {                    // steps every lane of both groups takes
+                const double va = pa[32 * k], vb = pb[32 * k];
+                const unsigned xa = ca[32 * k], xb = cb[32 * k];
+                ra = __dadd_rn(ra, __dmul_rn(va, in.xf(xs[xa], 0)));                    // csr_matvec order
+                rb = __dadd_rn(rb, __dmul_rn(vb, in.xf(xs[xb], 0)));
             }
-            acc[i][0] = ra;
-            acc[i][1] = rb;
+            for (; k < maxa; ++k) {                    // the rest: zero-filled entries are read and dropped
+                const double t = __dadd_rn(ra, __dmul_rn(pa[32 * k], in.xf(xs[ca[32 * k]], 0)));
+                ra = k < la ? t : ra;
+            }
+            for (k = both; k < maxb; ++k) {
+                const double t = __dadd_rn(rb, __dmul_rn(pb[32 * k], in.xf(xs[cb[32 * k]], 0)));
+                rb = k < lb ? t : rb;
+            }
+            if (la) sums[ra_i] = ra;
+            if (lb) sums[rb_i] = rb;
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
             if (++s == R.ns) { s = 0; ph ^= 1; }
@@ -302,13 +210,10 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
         consumer_sync(NC);                          // every consumer warp is done with window buffer j & 1
         if (tid == 0 && j + 2 < npass) issue(j + 2);
     }
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const long long r = row0 + i * 1024 + h * NC + tid;
-            if (r < n) out[r] = acc[i][h];
-        }
+    const long long row0 = (long long)blockIdx.x * RB;
+    for (int t = tid; t < RB; t += NC) {
+        const long long r = row0 + t;
+        if (r < n) out[r] = sums[t];
     }
 }
 

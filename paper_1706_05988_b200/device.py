@@ -133,34 +133,43 @@ def gather_mode():
     return mode
 
 
-# Shared-memory-window SpMV (kpl_op.bd_*, csrc/kpl_spmv_band.cuh).  Two windows
-# of the input vector live in shared memory: 16 bytes per window column.
-_BAND_W_MAX = 14336                  # 2 x 112 KiB of the 227 KiB a CTA may use
+# Shared-memory-window SpMV (kpl_op.bd_*, csrc/kpl_spmv_band.cuh).  A CTA's shared
+# memory holds the running sums of its super-block (8 B per row), two windows of
+# the input vector (16 B per window column) and a ring of matrix-stream slots.
+_BAND_SMEM = 227 * 1024
 _BAND_MIN_LINES = 12.0               # auto: CSR-order warp gathers touching >= 12 lines ...
 _BAND_MIN_ROW_NNZ = 16.0             # ... on rows longer than 16 nonzeros on average
-_BAND_MAX_LEN_BYTES = 0.25           # the per-(row, pass) length bytes stay under 25 % of the 10 B/nnz stream
+_BAND_MAX_DESC_BYTES = 0.35          # the 3 B per (row, pass) descriptors stay under 35 % of the 10 B/nnz stream
+_BAND_ROWS_MAX = 4608                # super-block height: 36 KiB of running sums at most
+_BAND_WINDOWS = (8192, 7168, 6144, 5120, 4096, 3072, 2048)
 _SMS = 148
 
 
-def band_rows_per_thread(n):
-    """Super-block height / 1024: the value in 4..7 whose CTA count fills whole
-    waves of 148 SMs best (ties: the taller block); small matrices: one wave."""
-    if n <= 4 * 1024 * _SMS:
-        return max(1, min(4, -(-n // (1024 * _SMS))))
-    best = None
-    for rpt in (7, 6, 5, 4):
-        nsb = -(-n // (1024 * rpt))
-        eff = nsb / (-(-nsb // _SMS) * _SMS)
-        if best is None or eff > best[0] + 1e-12:
-            best = (eff, rpt)
-    return best[1]
+def band_rows(n):
+    """Super-block height (a multiple of 32, <= 4608): the tallest whose CTA count is a
+    whole number of waves of 148 SMs (one CTA per SM); small matrices: one wave."""
+    waves = 1
+    while True:
+        rb = -(-n // (waves * _SMS))
+        rb = -(-rb // 32) * 32
+        if rb <= _BAND_ROWS_MAX:
+            return max(32, rb)
+        waves += 1
 
 
-def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, window=None, rpt=None):
-    """(bd_val, bd_col, bd_len, bd_grp, bd_sb, rpt, W, round_max) or None -- the layout
-    include/kpl_b200.h documents under kpl_op.bd_*.  Index work only (values are
-    permuted, never combined), done once per matrix with torch sorts on the
-    device the CSR arrays live on."""
+def band_ring_slots(rows, W, round_max):
+    """Ring slots csr_band_ring_spmv gets next to the sums and the two windows
+    (kpl_capi.cu:band_ring computes the same)."""
+    cap = (round_max + 63) // 64 * 64
+    room = _BAND_SMEM - 8 * rows - 16 * W - 128
+    return max(0, min(4, room // (10 * cap + 3 * 1024 + 144)))
+
+
+def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, window=None, rows=None):
+    """(bd_val, bd_col, bd_row, bd_len, bd_grp, bd_sb, rows, W, round_max) or None --
+    the layout include/kpl_b200.h documents under kpl_op.bd_*.  Index work only (the
+    values are permuted, never combined), done once per matrix with torch on the device
+    the CSR arrays live on."""
     mode = gather_mode() if mode is None else mode
     if mode in ("csr", "sorted"):
         return None
@@ -171,17 +180,17 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
         return None
     if mode == "auto" and (nnz < _BAND_MIN_ROW_NNZ * n or csr_lines_per_warp(col_idx_h) < _BAND_MIN_LINES):
         return None
-    rpt = int(rpt or int(os.environ.get("KPL_BAND_RPT", 0)) or band_rows_per_thread(n))
-    if not 1 <= rpt <= 8:
-        raise ValueError("window SpMV: rows per thread must be in 1..8")
-    RB = 1024 * rpt
-    G = RB // 32
+    RB = int(rows or int(os.environ.get("KPL_BAND_ROWS", 0)) or band_rows(n))
+    if RB < 32 or RB % 32 or RB > _BAND_ROWS_MAX:
+        raise ValueError(f"window SpMV: super-block height {RB} (expected a multiple of 32 in 32..{_BAND_ROWS_MAX})")
+    RP = -(-RB // 1024)                  # rounds (1024 slots = 32 groups) per pass
+    RBP = 1024 * RP                      # slots per pass (the tail slots are empty)
     nsb = -(-n // RB)
     dev = row_ptr.device
     counts = (row_ptr[1:] - row_ptr[:-1]).long()
-    rows = t.repeat_interleave(t.arange(n, device=dev), counts)
-    sb = rows // RB
-    lrow = rows - sb * RB
+    rowid = t.repeat_interleave(t.arange(n, device=dev), counts)
+    sb = rowid // RB
+    lrow = rowid - sb * RB
     col = col_idx.long()
     big = t.iinfo(t.int64).max
     c_lo = t.full((nsb,), big, dtype=t.int64, device=dev).scatter_reduce_(0, sb, col, "amin", include_self=True)
@@ -191,74 +200,82 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
     rel = col - c_lo[sb]
 
     def plan(W):
-        """Passes of window length W: (passes per super-block, first pass, total, pass of
-        every nonzero, (pass, row) lengths, most nonzeros in one round of 32 groups)."""
+        """Passes of window length W; None when the pass table gets too large."""
         npass = (c_hi - c_lo) // W + 1
         pass0 = t.cumsum(npass, 0) - npass
         NP = int(npass.sum())
-        if NP * RB >= 2**31:
+        if NP * RBP >= 2**31:
             return None
         p = pass0[sb] + rel // W
-        lens = t.bincount(p * RB + lrow, minlength=NP * RB)
-        round_max = int(lens.view(NP * rpt, 1024).sum(1).max())
-        return npass, pass0, NP, p, lens, round_max
+        lens = t.zeros(NP * RBP, dtype=t.int64, device=dev)
+        lens.scatter_add_(0, p * RBP + lrow, t.ones_like(p))
+        # slots of a pass: rows by length, longest first (stable); groups of 32 slots are
+        # dealt to the pass's RP rounds in turn, so every round holds a mix of lengths
+        ls, perm = t.sort(lens.view(NP, RBP), dim=1, descending=True, stable=True)
+        gmax = ls.view(NP, RBP // 32, 32)[:, :, 0]                    # longest row of each group
+        g = t.arange(RBP // 32, device=dev)
+        rnd, m = g % RP, g // RP                                      # sorted group g -> round, position
+        m = (m + 5 * rnd) % 32                                        # rotate: a warp sees every length class
+        ring_g = rnd * 32 + m                                         # group index in ring order
+        round_max = int(t.zeros(NP, RP, dtype=t.int64, device=dev).scatter_add_(
+            1, rnd.expand(NP, -1), gmax * 32).max())
+        return npass, pass0, NP, p, ls, perm, gmax, ring_g, round_max
 
     explicit = window or os.environ.get("KPL_BAND_W")
     if explicit:
         W = int(explicit)
-        if W < 2 or W % 2 or W > _BAND_W_MAX:
-            raise ValueError(f"window SpMV: window length {W} (expected an even value in 2..{_BAND_W_MAX})")
+        if W < 2 or W % 2 or W > 65536:
+            raise ValueError(f"window SpMV: window length {W} (expected an even value in 2..65536)")
         pl = plan(W)
+        if pl is None or band_ring_slots(RB, W, pl[8]) < 2:
+            return None
     else:
-        # the widest window that leaves room for four ring slots of the matrix stream
-        # (csr_band_ring_spmv; config 5: 8192 columns, 0.270 ms/iteration against 0.287 with
-        # two slots at 10240); failing that, the plain-load kernel with the widest window
+        # the widest window that leaves room for three ring slots of the matrix stream
         pl = None
-        for W in _BAND_RING_WINDOWS:
+        for W in _BAND_WINDOWS:
             pl = plan(W)
-            if pl is not None and band_ring_slots(W, pl[5]) >= 4:
+            if pl is not None and band_ring_slots(RB, W, pl[8]) >= 3:
                 break
         else:
-            W = _BAND_W_MAX
-            pl = plan(W)
-    if pl is None:
-        return None
-    npass, pass0, NP, p, lens, round_max = pl
-    if mode == "auto" and NP * RB > _BAND_MAX_LEN_BYTES * 10.0 * nnz:
+            return None
+    npass, pass0, NP, p, ls, perm, gmax, ring_g, round_max = pl
+    if mode == "auto" and 3.0 * NP * RBP > _BAND_MAX_DESC_BYTES * 10.0 * nnz:
         return None                                                   # too wide a span for the window walk
-    if int(lens.max()) > 255:
+    if int(ls.max()) > 255:
         return None
-    bcol = rel - (rel // W) * W
-    # CSR order is (row, column) and the pass grows with the column, so the entry's rank
-    # inside its (pass, row) segment follows from a stable sort by (pass, row)
-    slot = p * RB + lrow
-    order = t.argsort(slot, stable=True)                              # (pass, row, column)
-    seg_start = t.cumsum(lens, 0) - lens
-    k = t.empty_like(order)
-    k[order] = t.arange(nnz, device=dev) - seg_start[slot[order]]
-    key = ((p * G + lrow // 32) * 256 + k) * 32 + lrow % 32           # (pass, group, step, lane)
-    perm = t.argsort(key)
-    del key, k, order, seg_start, slot
-    pad = lambda a: t.cat([a, a.new_zeros(8)])                        # bulk copies widen to 16-byte bounds
-    bd_val = pad(values[perm])
-    bd_col = pad(bcol[perm].to(t.int32).to(t.int16))                  # < 65536: uint16 bits
-    bd_len = lens.to(t.uint8)
-    gtot = lens.view(NP * G, 32).sum(1)
-    bd_grp = t.full((NP * G + 8,), nnz, dtype=t.int32, device=dev)    # terminal entry + bulk-copy slack
-    bd_grp[0] = 0
-    bd_grp[1:NP * G + 1] = t.cumsum(gtot, 0).to(t.int32)
+    G = RBP // 32
+    # ring-order slot of every sorted slot, and the reverse map row -> slot
+    spos = t.arange(RBP, device=dev)
+    ring_slot = ring_g[spos // 32] * 32 + spos % 32                   # sorted position -> ring-order slot
+    bd_row = t.empty(NP, RBP, dtype=t.int64, device=dev)
+    bd_len = t.empty(NP, RBP, dtype=t.int64, device=dev)
+    bd_row[:, ring_slot] = perm
+    bd_len[:, ring_slot] = ls
+    slot_of_row = t.empty(NP, RBP, dtype=t.int64, device=dev)
+    slot_of_row.scatter_(1, perm, ring_slot.expand(NP, -1))
+    # groups in ring order: each stored as (its longest row) full steps of 32 entries
+    gsz = t.empty(NP, G, dtype=t.int64, device=dev)
+    gsz[:, ring_g] = gmax * 32
+    gstart = t.cumsum(gsz.view(-1), 0) - gsz.view(-1)
+    S = int(gsz.sum())
+    if S + 64 >= 2**31:
+        return None
+    # the k-th nonzero of a (pass, row) segment: segments are contiguous in CSR order
+    idx = t.arange(nnz, device=dev)
+    first = t.ones(nnz, dtype=t.bool, device=dev)
+    first[1:] = (rowid[1:] != rowid[:-1]) | (p[1:] != p[:-1])
+    k = idx - t.cummax(t.where(first, idx, t.zeros_like(idx)), 0)[0]
+    slot = slot_of_row.view(-1)[p * RBP + lrow]
+    pos = gstart[p * G + slot // 32] + k * 32 + slot % 32
+    bd_val = values.new_zeros(S + 64)
+    bd_col = t.zeros(S + 64, dtype=t.int16, device=dev)
+    bd_val[pos] = values
+    bd_col[pos] = (rel - (rel // W) * W).to(t.int32).to(t.int16)      # < 65536: uint16 bits
+    bd_grp = t.full((NP * G + 8,), S, dtype=t.int32, device=dev)      # terminal entry + bulk-copy slack
+    bd_grp[:NP * G] = gstart.to(t.int32)
     bd_sb = t.stack([pass0, npass, c_lo, t.zeros_like(c_lo)], 1).to(t.int32).contiguous()
-    return bd_val, bd_col, bd_len, bd_grp, bd_sb, rpt, W, round_max
-
-
-_BAND_RING_WINDOWS = (8192, 7168, 6144, 5120, 4096)
-
-
-def band_ring_slots(W, round_max):
-    """Ring slots csr_band_ring_spmv gets next to two windows of W columns
-    (kpl_capi.cu:band_ring; < 2: the plain-load kernel runs instead)."""
-    cap = (round_max + 16 + 63) // 64 * 64
-    return min(4, (227 * 1024 - 16 * W - 128) // (10 * cap + 1024 + 144))
+    return (bd_val, bd_col, bd_row.view(-1).to(t.int32).to(t.int16).contiguous(),
+            bd_len.view(-1).to(t.uint8).contiguous(), bd_grp, bd_sb, RB, W, round_max)
 
 
 # Column-sorted SpMV gathers (kpl_op.sp_*): meant for matrices whose CSR-order
@@ -449,9 +466,10 @@ def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk
             op.sp_col, op.sp_val, op.sp_dest = ptr(sc), ptr(sv), ptr(sd)
             op.sp_rows, op.sp_max = R, most
         if dm.band is not None:
-            bv, bc, bl, bg, bs, rpt, W, round_max = dm.band
-            op.bd_val, op.bd_col, op.bd_len, op.bd_grp, op.bd_sb = ptr(bv), ptr(bc), ptr(bl), ptr(bg), ptr(bs)
-            op.bd_rpt, op.bd_w, op.bd_round_max = rpt, W, round_max
+            bv, bc, br, bl, bg, bs, rows, W, round_max = dm.band
+            op.bd_val, op.bd_col, op.bd_row, op.bd_len = ptr(bv), ptr(bc), ptr(br), ptr(bl)
+            op.bd_grp, op.bd_sb = ptr(bg), ptr(bs)
+            op.bd_rows, op.bd_w, op.bd_round_max = rows, W, round_max
     op.zc = zc
     op.vx = vx
     op.chunk_blocks = chunk_blocks

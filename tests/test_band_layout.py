@@ -12,36 +12,48 @@ from paper_1706_05988_b200.sparse import SparseMatrix
 
 
 def walk(layout, n, x):
-    """What csr_band_spmv computes, one (super-block, pass, group, lane) at a time."""
-    val, col, ln, grp, sb, rpt, W, round_max = layout
-    val, col = val.numpy(), col.numpy().view(np.uint16)
+    """What csr_band_ring_spmv computes, one (super-block, pass, group, lane) at a time."""
+    val, col, row, ln, grp, sb, RB, W, round_max = layout
+    val, col, row = val.numpy(), col.numpy().view(np.uint16), row.numpy().view(np.uint16)
     ln, grp, sb = ln.numpy(), grp.numpy(), sb.numpy()
-    RB, G = 1024 * rpt, 32 * rpt
+    RP = -(-RB // 1024)
+    RBP, G = 1024 * RP, 32 * RP
     out = np.zeros(n)
+    seen = 0
     for s in range(sb.shape[0]):
         pass0, npass, c_lo, _ = (int(v) for v in sb[s])
         acc = np.zeros(RB)                         # +0.0, as the reference's accumulator
         for j in range(npass):
             p = pass0 + j
             w0 = c_lo + j * W
-            for g in range(G):
-                lens = ln[p * RB + 32 * g: p * RB + 32 * g + 32].astype(np.int64)
-                base = int(grp[p * G + g])
-                for k in range(int(lens.max(initial=0))):
-                    lanes = np.nonzero(lens > k)[0]
-                    for rank, lane in enumerate(lanes):
-                        e = base + rank
-                        c = w0 + int(col[e])
-                        assert c < n and int(col[e]) < W
-                        acc[32 * g + lane] = acc[32 * g + lane] + val[e] * x[c]
-                    base += len(lanes)
-                assert base == int(grp[p * G + g + 1])
-            for i in range(rpt):
-                assert int(grp[p * G + 32 * i + 32]) - int(grp[p * G + 32 * i]) <= round_max
+            rows_seen = []
+            for i in range(RP):
+                e0 = int(grp[p * G + 32 * i])
+                assert int(grp[p * G + 32 * i + 32]) - e0 <= round_max
+                for g in range(32 * i, 32 * i + 32):
+                    lens = ln[p * RBP + 32 * g: p * RBP + 32 * g + 32].astype(np.int64)
+                    rws = row[p * RBP + 32 * g: p * RBP + 32 * g + 32].astype(np.int64)
+                    base = int(grp[p * G + g])
+                    L = int(lens.max(initial=0))
+                    assert L == int(lens[0]) and base % 32 == 0      # longest row first
+                    assert np.all(np.diff(lens) <= 0)
+                    assert int(grp[p * G + g + 1]) - base == 32 * L
+                    for k in range(L):
+                        for lane in range(32):
+                            e = base + 32 * k + lane
+                            if lens[lane] > k:
+                                c = w0 + int(col[e])
+                                assert c < n and int(col[e]) < W and rws[lane] < RB
+                                acc[rws[lane]] = acc[rws[lane]] + val[e] * x[c]
+                                seen += 1
+                            else:
+                                assert val[e] == 0.0 and col[e] == 0    # zero fill past the row's end
+                    rows_seen.extend(rws[lens > 0].tolist())
+            assert len(rows_seen) == len(set(rows_seen))              # a row has one slot per pass
         r0 = s * RB
         m = min(RB, n - r0)
         out[r0:r0 + m] = acc[:m]
-    return out
+    return out, seen
 
 
 def build(A, **kw):
@@ -51,18 +63,17 @@ def build(A, **kw):
     return D.band_layout(A.row_ptr, A.col_idx, rp, ci, va, **kw)
 
 
-@pytest.mark.parametrize("n,band,window,rpt", [(3000, 300, 64, 1), (2500, 2400, 128, 2), (1500, 40, 14336, 1),
-                                                (1025, 500, 2, 1)])
-def test_band_layout_walk_equals_csr_matvec(n, band, window, rpt):
+@pytest.mark.parametrize("n,band,window,rows", [(3000, 300, 64, 1024), (2500, 2400, 128, 1056), (1500, 40, 8192, 32),
+                                                 (1025, 500, 2, 544), (5000, 900, 256, 2400)])
+def test_band_layout_walk_equals_csr_matvec(n, band, window, rows):
     A = problems.banded_spd(n, seed=3, per_row=6, band=band)
-    lay = build(A, mode="band", window=window, rpt=rpt)
+    lay = build(A, mode="band", window=window, rows=rows)
     assert lay is not None
     x = np.random.default_rng(5).standard_normal(n)
     ref = O.spmv(O.as_oracle_operator(A), x)
-    assert walk(lay, n, x).tobytes() == ref.tobytes()
-    # every nonzero is stored exactly once
-    assert int(lay[3][-8]) == len(A.values) and int(lay[3][-1]) == len(A.values)
-    assert np.array_equal(np.sort(lay[0].numpy()[:-8]), np.sort(A.values))
+    got, seen = walk(lay, n, x)
+    assert got.tobytes() == ref.tobytes()
+    assert seen == len(A.values)                                      # every nonzero exactly once
 
 
 def test_band_layout_handles_empty_rows_and_negative_zero():
@@ -74,11 +85,11 @@ def test_band_layout_handles_empty_rows_and_negative_zero():
     cols = np.array([0, 900, 3, 5, 1000, 2, 1099])
     vals = np.array([1.0, -2.0, 0.5, 4.0, -1.0, -0.0, 3.0])
     A = SparseMatrix(n, row_ptr, cols, vals, check_symmetry=False)
-    lay = build(A, mode="band", window=32, rpt=1)
+    lay = build(A, mode="band", window=32, rows=512)
     x = -np.ones(n)
     x[2] = 0.0
     ref = O.spmv(O.as_oracle_operator(A), x)
-    assert walk(lay, n, x).tobytes() == ref.tobytes()
+    assert walk(lay, n, x)[0].tobytes() == ref.tobytes()
 
 
 def test_band_layout_auto_rules():
@@ -89,5 +100,5 @@ def test_band_layout_auto_rules():
     # a scattered band does
     B = problems.banded_spd(6000, seed=0, per_row=11, band=2000)
     assert build(B, mode="auto") is not None
-    assert D.band_rows_per_thread(2_000_000) == 7
-    assert D.band_rows_per_thread(20_000) == 1
+    assert D.band_rows(2_000_000) == 4512        # 444 CTAs = 3 waves of 148
+    assert D.band_rows(20_000) == 160            # one wave

@@ -60,15 +60,14 @@ def test_spmv_layouts_bitwise(monkeypatch, name, make):
     assert same_bits(outs["csr"], outs["band"])
 
 
-@pytest.mark.parametrize("kernel", ["ring", "ldg"])
-@pytest.mark.parametrize("window,rpt", [(2, 1), (64, 1), (1000, 2), (4096, 3), (9216, 7), (14336, 8), (14336, 0)])
-def test_band_windows_and_block_heights_bitwise(monkeypatch, window, rpt, kernel):
-    """Many short passes, odd window tails (n odd), every super-block height; the
-    ring-fed kernel (bulk copies of the matrix stream) and the plain-load one."""
+@pytest.mark.parametrize("window,rows", [(2, 32), (64, 1024), (1000, 1056), (4096, 2400), (8192, 2400), (6144, 0),
+                                         (512, 3072)])
+def test_band_windows_and_block_heights_bitwise(monkeypatch, window, rows):
+    """Many short passes, odd window tails (n odd), super-block heights that are and are
+    not multiples of the 1024-slot rounds."""
     monkeypatch.setenv("KPL_CSR_GATHER", "band")
-    monkeypatch.setenv("KPL_BAND_KERNEL", kernel)
     monkeypatch.setenv("KPL_BAND_W", str(window))
-    monkeypatch.setenv("KPL_BAND_RPT", str(rpt))
+    monkeypatch.setenv("KPL_BAND_ROWS", str(rows))
     A = problems.banded_spd(9_001 if window <= 64 else 70_001, seed=window, band=700 if window <= 64 else 30_000)
     v = np.random.default_rng(11).standard_normal(A.n)
     v[::3] = -0.0
@@ -76,7 +75,7 @@ def test_band_windows_and_block_heights_bitwise(monkeypatch, window, rpt, kernel
     B = fresh(A)
     got = np.asarray(K.spmv(B, v))
     lay = D.device_matrix(B, D.require_cuda()).band
-    assert lay is not None and lay[6] == window and (rpt == 0 or lay[5] == rpt)
+    assert lay is not None and lay[7] == window and (rows == 0 or lay[6] == rows)
     assert same_bits(got, want), first_diff(got, want)
 
 
