@@ -59,7 +59,7 @@ BandRing band_ring(const kpl_op *op) {
     BandRing r{0, 0};
     r.cap = (op->bd_round_max + 63) / 64 * 64;
     const long long room = 227LL * 1024 - 8LL * op->bd_rows - 16LL * op->bd_w - 128;
-    r.ns = (int)std::max<long long>(0, std::min<long long>(4, room / (long long)r.slot()));
+    r.ns = (int)std::max<long long>(0, std::min<long long>(12, room / (long long)r.slot()));
     return r;
 }
 

@@ -162,7 +162,7 @@ def band_ring_slots(rows, W, round_max):
     (kpl_capi.cu:band_ring computes the same)."""
     cap = (round_max + 63) // 64 * 64
     room = _BAND_SMEM - 8 * rows - 16 * W - 128
-    return max(0, min(4, room // (10 * cap + 3 * 1024 + 144)))
+    return max(0, min(12, room // (10 * cap + 3 * 1024 + 144)))
 
 
 def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, window=None, rows=None):
@@ -230,11 +230,13 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
         if pl is None or band_ring_slots(RB, W, pl[8]) < 2:
             return None
     else:
-        # the widest window that leaves room for three ring slots of the matrix stream
+        # the widest window that leaves room for two ring slots of the matrix stream (config 5,
+        # ms/iteration: 8192 columns 0.260, 6144 0.266, 4096 0.286, 2048 0.412 -- passes cost more
+        # than ring depth gains)
         pl = None
         for W in _BAND_WINDOWS:
             pl = plan(W)
-            if pl is not None and band_ring_slots(RB, W, pl[8]) >= 3:
+            if pl is not None and band_ring_slots(RB, W, pl[8]) >= 2:
                 break
         else:
             return None
