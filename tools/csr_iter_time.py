@@ -65,6 +65,19 @@ def main():
             S.iterate(1)
             torch.cuda.synchronize()
         print(name, tag, f"{best:.4f} ms/iteration (best of 3 x 9)", flush=True)
+        if os.environ.get("KPL_LONG"):
+            # sustained: 400 iterations with the true-residual cadence, one enqueue
+            S = _Solve(A, M, b, None, K.SolverConfig(method="pcg_sh", shift=0.4, max_iters=1000), chunk_blocks=cb)
+            S.init()
+            S.iterate(10)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            S.iterate(400)
+            e1.record()
+            torch.cuda.synchronize()
+            print(name, tag, f"{e0.elapsed_time(e1) / 400:.4f} ms/iteration sustained (400 iterations incl. cadence)",
+                  flush=True)
 
 
 if __name__ == "__main__":
