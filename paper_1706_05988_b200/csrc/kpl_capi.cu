@@ -828,6 +828,9 @@ int do_sweep(const Ctx &c, int kind, long long row) {
     int phase, pred;
     int rc = kind_phase(kind, phase, pred);
     if (rc != KPL_OK) return rc;
+    // only p-CG-rr ever raises `fire`: the other methods skip the second head load every CTA
+    // would make before it starts (a serial L2 round trip per CTA: config 4 0.875 -> 0.78 ms/iteration)
+    if (pred == PRED_NOFIRE && c.cfg.method != KPL_M_PCG_RR) pred = PRED_RUNNING;
     const bool tma = tma_eligible(op, L);
     const double *u = c.ident ? v->r : v->u;
     switch (kind) {
@@ -1276,6 +1279,7 @@ int kpl_finalize_global(const kpl_op *op, const kpl_cfg *cfgp, int32_t kind, int
     if ((rc = kind_phase(kind, phase, pred)) != KPL_OK) return rc;
     if (phase == PH_NONE) return KPL_OK;
     const Cfg cfg = make_cfg(cfgp);
+    if (pred == PRED_NOFIRE && cfg.method != KPL_M_PCG_RR) pred = PRED_RUNNING;
     const Ws ws = make_ws(op, L, cfg.max_iters, workspace);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     finalize_kernel<<<1, NT, 0, (cudaStream_t)stream>>>(ws, cfg, phase, pred, row);
@@ -1385,6 +1389,7 @@ int kpl_peer_finalize(const kpl_op *op, const kpl_cfg *cfgp, int32_t kind, int64
     if (kind != 0 && (rc = kind_phase(kind, phase, pred)) != KPL_OK) return rc;
     if (phase != PH_NONE && !table) return fail(KPL_EINVAL, "reducing sweep needs the exchange table");
     const Cfg cfg = make_cfg(cfgp);
+    if (pred == PRED_NOFIRE && cfg.method != KPL_M_PCG_RR) pred = PRED_RUNNING;
     Ws ws = make_ws(op, L, cfg.max_iters, workspace);
     if (table) ws.chunks = const_cast<double *>(table);
     g_launches.fetch_add(1, std::memory_order_relaxed);

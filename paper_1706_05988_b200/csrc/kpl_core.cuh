@@ -433,12 +433,15 @@ __device__ void finalize(const Ws &ws, const Cfg &cfg, int phase, const double (
 // Per-kernel uniform predicate.
 __device__ __forceinline__ bool pred_ok(const WsHead *h, int pred, long long row) {
     if (pred == PRED_ALWAYS) return true;          // (plain spmv launches carry no workspace)
+    // both words are requested before either is tested: one L2 round trip, not two in series
     const long long state = ld_head(&h->state);
+    const long long second = pred == PRED_ROW ? ld_head(&h->iter)
+                             : (pred == PRED_FIRE || pred == PRED_NOFIRE) ? ld_head(&h->fire) : 0;
     switch (pred) {
     case PRED_RUNNING: return state == KPL_ST_RUNNING;
-    case PRED_FIRE: return state == KPL_ST_RUNNING && ld_head(&h->fire) != 0;
-    case PRED_ROW: return ld_head(&h->iter) == row && state != KPL_ST_BREAKDOWN;
-    case PRED_NOFIRE: return state == KPL_ST_RUNNING && ld_head(&h->fire) == 0;
+    case PRED_FIRE: return state == KPL_ST_RUNNING && second != 0;
+    case PRED_ROW: return second == row && state != KPL_ST_BREAKDOWN;
+    case PRED_NOFIRE: return state == KPL_ST_RUNNING && second == 0;
     default: return true;
     }
 }
