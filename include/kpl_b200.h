@@ -115,9 +115,9 @@ typedef struct kpl_op {
     /* CSR, optional shared-memory-window layout of the SpMV for scattered
        banded matrices (NULL = not used; takes precedence over sp_*).  Rows are
        grouped in super-blocks of bd_rows rows, one CTA each.  Super-block s
-       walks its column span in bd_sb[4s+1] windows of bd_w columns starting at
-       column bd_sb[4s+2] (even); window j of super-block s is "pass"
-       p = bd_sb[4s] + j.  The CTA keeps the window's slice of the input vector
+       walks the bd_sb[4s+1] windows of bd_w columns in which its rows have
+       nonzeros, in ascending column order; its j-th window is "pass"
+       p = bd_sb[4s] + j and starts at column bd_win[p] (even).  The CTA keeps the window's slice of the input vector
        in shared memory (bulk copies, double-buffered), so the gathers are
        shared-memory loads, and the running sum of every row of the super-block
        in shared memory as well.
@@ -145,6 +145,7 @@ typedef struct kpl_op {
     int32_t bd_w;            /* window length in columns (even, <= 65536)         */
     int32_t bd_round_max;
     int32_t _reserved2;
+    const int32_t  *bd_win;  /* first column of every pass                        */
 } kpl_op;
 
 #define KPL_ORDER_TREE      0

@@ -45,7 +45,7 @@ class KplOp(ctypes.Structure):
                 ("ic_l_order", _p), ("ic_u_order", _p),
                 ("sp_col", _p), ("sp_val", _p), ("sp_dest", _p), ("sp_rows", _i32), ("sp_max", _i32),
                 ("bd_val", _p), ("bd_col", _p), ("bd_row", _p), ("bd_len", _p), ("bd_grp", _p), ("bd_sb", _p),
-                ("bd_rows", _i32), ("bd_w", _i32), ("bd_round_max", _i32), ("_reserved2", _i32)]
+                ("bd_rows", _i32), ("bd_w", _i32), ("bd_round_max", _i32), ("_reserved2", _i32), ("bd_win", _p)]
 
 
 class KplCfg(ctypes.Structure):

@@ -53,7 +53,8 @@ struct BandGeo {
     const unsigned short *rowi;
     const unsigned char *len;
     const int *grp;
-    const int4 *sb;           // {first pass, passes, first column (even), -}
+    const int4 *sb;           // {first pass, passes, -, -}
+    const int *win;           // first column of every pass (even)
     int W, rows;
 };
 
@@ -149,7 +150,7 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
     // (made visible by the release of the expect_tx arrive that follows it)
     auto issue = [&](int j) {
         double *dst = (j & 1) ? xs1 : xs0;
-        const long long w0 = info.z + (long long)j * B.W;
+        const long long w0 = __ldg(B.win + pass0 + j);
         const long long len = min((long long)B.W, n - w0);
         if (len & 1) dst[len - 1] = x[w0 + len - 1];
         const unsigned bytes = (unsigned)((len & ~1LL) * 8);

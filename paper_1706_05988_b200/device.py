@@ -166,7 +166,7 @@ def band_ring_slots(rows, W, round_max):
 
 
 def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, window=None, rows=None):
-    """(bd_val, bd_col, bd_row, bd_len, bd_grp, bd_sb, rows, W, round_max) or None --
+    """(bd_val, bd_col, bd_row, bd_len, bd_grp, bd_sb, rows, W, round_max, bd_win) or None --
     the layout include/kpl_b200.h documents under kpl_op.bd_*.  Index work only (the
     values are permuted, never combined), done once per matrix with torch on the device
     the CSR arrays live on."""
@@ -200,13 +200,17 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
     rel = col - c_lo[sb]
 
     def plan(W):
-        """Passes of window length W; None when the pass table gets too large."""
-        npass = (c_hi - c_lo) // W + 1
-        pass0 = t.cumsum(npass, 0) - npass
-        NP = int(npass.sum())
+        """Passes of window length W -- the windows of a super-block's span that hold
+        nonzeros of its rows, in ascending column order; None when the pass table gets too large."""
+        nwin = int(((c_hi - c_lo) // W + 1).max())
+        wkey, p = t.unique(sb * nwin + rel // W, return_inverse=True)    # sorted: (super-block, window)
+        NP = int(wkey.numel())
         if NP * RBP >= 2**31:
             return None
-        p = pass0[sb] + rel // W
+        psb = wkey // nwin
+        npass = t.bincount(psb, minlength=nsb)
+        pass0 = t.cumsum(npass, 0) - npass
+        win = c_lo[psb] + (wkey % nwin) * W                               # first column of every pass
         lens = t.zeros(NP * RBP, dtype=t.int64, device=dev)
         lens.scatter_add_(0, p * RBP + lrow, t.ones_like(p))
         # slots of a pass: rows by length, longest first (stable); groups of 32 slots are
@@ -219,7 +223,7 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
         ring_g = rnd * 32 + m                                         # group index in ring order
         round_max = int(t.zeros(NP, RP, dtype=t.int64, device=dev).scatter_add_(
             1, rnd.expand(NP, -1), gmax * 32).max())
-        return npass, pass0, NP, p, ls, perm, gmax, ring_g, round_max
+        return npass, pass0, NP, p, ls, perm, gmax, ring_g, round_max, win
 
     explicit = window or os.environ.get("KPL_BAND_W")
     if explicit:
@@ -240,7 +244,7 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
                 break
         else:
             return None
-    npass, pass0, NP, p, ls, perm, gmax, ring_g, round_max = pl
+    npass, pass0, NP, p, ls, perm, gmax, ring_g, round_max, win = pl
     if mode == "auto" and 3.0 * NP * RBP > _BAND_MAX_DESC_BYTES * 10.0 * nnz:
         return None                                                   # too wide a span for the window walk
     if int(ls.max()) > 255:
@@ -275,9 +279,9 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
     bd_col[pos] = (rel - (rel // W) * W).to(t.int32).to(t.int16)      # < 65536: uint16 bits
     bd_grp = t.full((NP * G + 8,), S, dtype=t.int32, device=dev)      # terminal entry + bulk-copy slack
     bd_grp[:NP * G] = gstart.to(t.int32)
-    bd_sb = t.stack([pass0, npass, c_lo, t.zeros_like(c_lo)], 1).to(t.int32).contiguous()
+    bd_sb = t.stack([pass0, npass, t.zeros_like(c_lo), t.zeros_like(c_lo)], 1).to(t.int32).contiguous()
     return (bd_val, bd_col, bd_row.view(-1).to(t.int32).to(t.int16).contiguous(),
-            bd_len.view(-1).to(t.uint8).contiguous(), bd_grp, bd_sb, RB, W, round_max)
+            bd_len.view(-1).to(t.uint8).contiguous(), bd_grp, bd_sb, RB, W, round_max, win.to(t.int32).contiguous())
 
 
 # Column-sorted SpMV gathers (kpl_op.sp_*): meant for matrices whose CSR-order
@@ -468,7 +472,8 @@ def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk
             op.sp_col, op.sp_val, op.sp_dest = ptr(sc), ptr(sv), ptr(sd)
             op.sp_rows, op.sp_max = R, most
         if dm.band is not None:
-            bv, bc, br, bl, bg, bs, rows, W, round_max = dm.band
+            bv, bc, br, bl, bg, bs, rows, W, round_max, bw = dm.band
+            op.bd_win = ptr(bw)
             op.bd_val, op.bd_col, op.bd_row, op.bd_len = ptr(bv), ptr(bc), ptr(br), ptr(bl)
             op.bd_grp, op.bd_sb = ptr(bg), ptr(bs)
             op.bd_rows, op.bd_w, op.bd_round_max = rows, W, round_max

@@ -13,7 +13,8 @@ from paper_1706_05988_b200.sparse import SparseMatrix
 
 def walk(layout, n, x):
     """What csr_band_ring_spmv computes, one (super-block, pass, group, lane) at a time."""
-    val, col, row, ln, grp, sb, RB, W, round_max = layout
+    val, col, row, ln, grp, sb, RB, W, round_max, win = layout
+    win = win.numpy()
     val, col, row = val.numpy(), col.numpy().view(np.uint16), row.numpy().view(np.uint16)
     ln, grp, sb = ln.numpy(), grp.numpy(), sb.numpy()
     RP = -(-RB // 1024)
@@ -21,11 +22,13 @@ def walk(layout, n, x):
     out = np.zeros(n)
     seen = 0
     for s in range(sb.shape[0]):
-        pass0, npass, c_lo, _ = (int(v) for v in sb[s])
+        pass0, npass = int(sb[s][0]), int(sb[s][1])
         acc = np.zeros(RB)                         # +0.0, as the reference's accumulator
         for j in range(npass):
             p = pass0 + j
-            w0 = c_lo + j * W
+            w0 = int(win[p])
+            assert w0 % 2 == 0 and (j == 0 or w0 > int(win[p - 1]))         # ascending windows
+            assert int(ln[p * RBP:(p + 1) * RBP].sum()) > 0                   # no empty pass is stored
             rows_seen = []
             for i in range(RP):
                 e0 = int(grp[p * G + 32 * i])
