@@ -104,3 +104,21 @@ def test_solves_identical_across_layouts(monkeypatch, method, extra):
     # and both are the oracle run in the device's reduction order
     ores = O.solve(A, O.make_jacobi(O.as_oracle_operator(A)), b, None, O.Config(**kw), dot=gpu_dot(A))
     assert same_bits(hist6(res["sorted"]), oracle_hist6(ores))
+
+
+def test_band_falls_back_for_inputs_bulk_copies_cannot_take(monkeypatch):
+    """An input vector at an address that is not a multiple of 16 bytes cannot be bulk-copied
+    into the window buffers: the CSR-order kernel runs instead, same bits."""
+    monkeypatch.setenv("KPL_CSR_GATHER", "band")
+    A = problems.banded_spd(30_001, seed=9, band=5000)
+    B = fresh(A)
+    rng = np.random.default_rng(3)
+    host = rng.standard_normal(A.n + 1)
+    dev = torch.as_tensor(host, device="cuda")
+    assert D.device_matrix(B, D.require_cuda()).band is not None
+    for off in (0, 1):                       # 16-byte aligned, then 8 bytes off
+        v = dev[off:off + A.n]
+        assert v.data_ptr() % 16 == 8 * off
+        got = K.spmv(B, v).cpu().numpy()
+        want = O.spmv(O.as_oracle_operator(A), host[off:off + A.n])
+        assert same_bits(got, want), (off, first_diff(got, want))
