@@ -117,35 +117,37 @@ typedef struct kpl_op {
        grouped in super-blocks of bd_rows rows, one CTA each.  Super-block s
        walks the bd_sb[4s+1] windows of bd_w columns in which its rows have
        nonzeros, in ascending column order; its j-th window is "pass"
-       p = bd_sb[4s] + j and starts at column bd_win[p] (even).  The CTA keeps the window's slice of the input vector
-       in shared memory (bulk copies, double-buffered), so the gathers are
-       shared-memory loads, and the running sum of every row of the super-block
-       in shared memory as well.
-       A pass has RBP = 1024*ceil(bd_rows/1024) slots; slot t of pass p works on
-       local row bd_row[p*RBP + t], which has bd_len[p*RBP + t] (<= 255) nonzeros
-       inside the window.  Slots are ordered so that the 32 slots of a group
-       hold rows of (nearly) equal length, longest first, and the groups of a
-       pass are dealt to its ceil(bd_rows/1024) rounds of 32 groups in turn.
-       Group g (32 slots 32g..32g+31, counted over all passes) stores L full
-       steps of 32 entries from bd_grp[g] on (L = its longest row; entry 32k+l
-       is the k-th nonzero of slot l's row, zero-filled past the row's end):
-       bd_val / bd_col hold the values and the columns relative to the window
-       start (uint16).  A lane adds its row's products to the row's running sum
-       left to right, pass after pass, i.e. in ascending column order from
-       +0.0: the csr_matvec order (_kernels.py:44-52), bit for bit.
-       bd_round_max = most entries in one round.  Padding: 64 spare entries
-       after bd_val / bd_col, 8 spare ints after bd_grp (bulk copies).        */
-    const double   *bd_val;
-    const uint16_t *bd_col;
-    const uint16_t *bd_row;
-    const uint8_t  *bd_len;
-    const int32_t  *bd_grp;
+       p = bd_sb[4s] + j and starts at column bd_win[p] (even).  The CTA keeps
+       the window's slice of the input vector in shared memory (bulk copies,
+       double-buffered), so the gathers are shared-memory loads, and the
+       running sum of every row of the super-block in shared memory as well.
+       A pass has RBP = 1024*ceil(bd_rows/1024) slots, one per local row (the
+       tail slots are empty), ordered so that the 32 slots of a group hold rows
+       with (nearly) the same number of nonzeros inside the window, longest
+       first; the groups of a pass are dealt to its RBP/1024 rounds of 32
+       groups in turn.  The matrix is stored as one byte stream of round
+       records, one bulk copy each; round r (counted over all passes) is
+       bytes 16*bd_roff[r] .. 16*bd_roff[r+1] of bd_stream:
+           int32  grp[36]    first entry of each of the 32 groups, then the end
+                             (absolute entry numbers; 3 unused), 16 bytes pad
+           uint8  len[1024]  nonzeros of the slot's row inside the window (<= 255)
+           uint16 row[1024]  the slot's local row
+           uint16 col[cnt]   entry columns relative to the window start
+           double val[cnt]   entry values            (cnt = grp[32] - grp[0])
+       A group stores L full steps of 32 entries (L = its longest row; entry
+       32k+l is the k-th nonzero of slot l's row, zero-filled past the row's
+       end).  A lane adds its row's products to the row's running sum left to
+       right, pass after pass, i.e. in ascending column order from +0.0: the
+       csr_matvec order (_kernels.py:44-52), bit for bit.
+       bd_round_max = most entries in one round.                              */
+    const uint8_t  *bd_stream;
+    const int32_t  *bd_roff;
     const int32_t  *bd_sb;
+    const int32_t  *bd_win;  /* first column of every pass                        */
     int32_t bd_rows;         /* rows per super-block (multiple of 32, <= 4608)    */
     int32_t bd_w;            /* window length in columns (even, <= 65536)         */
     int32_t bd_round_max;
     int32_t _reserved2;
-    const int32_t  *bd_win;  /* first column of every pass                        */
 } kpl_op;
 
 #define KPL_ORDER_TREE      0

@@ -44,8 +44,8 @@ class KplOp(ctypes.Structure):
                 ("ic_u_row_ptr", _p), ("ic_u_col_idx", _p), ("ic_u_values", _p),
                 ("ic_l_order", _p), ("ic_u_order", _p),
                 ("sp_col", _p), ("sp_val", _p), ("sp_dest", _p), ("sp_rows", _i32), ("sp_max", _i32),
-                ("bd_val", _p), ("bd_col", _p), ("bd_row", _p), ("bd_len", _p), ("bd_grp", _p), ("bd_sb", _p),
-                ("bd_rows", _i32), ("bd_w", _i32), ("bd_round_max", _i32), ("_reserved2", _i32), ("bd_win", _p)]
+                ("bd_stream", _p), ("bd_roff", _p), ("bd_sb", _p), ("bd_win", _p),
+                ("bd_rows", _i32), ("bd_w", _i32), ("bd_round_max", _i32), ("_reserved2", _i32)]
 
 
 class KplCfg(ctypes.Structure):

@@ -104,7 +104,7 @@ int make_layout(const kpl_op *op, Layout &L) {
         if (op->sp_col && (!op->sp_val || !op->sp_dest || op->sp_rows < 1 || op->sp_max < 1 ||
                            op->sp_max > 65535 || 8LL * op->sp_max > 227 * 1024))
             return fail(KPL_EINVAL, "bad column-sorted SpMV layout");
-        if (op->bd_val && (!op->bd_col || !op->bd_row || !op->bd_len || !op->bd_grp || !op->bd_sb || !op->bd_win ||
+        if (op->bd_stream && (!op->bd_roff || !op->bd_sb || !op->bd_win ||
                            op->bd_rows < 32 || op->bd_rows % 32 || op->bd_rows > 4608 || op->bd_w < 2 ||
                            (op->bd_w & 1) || op->bd_w > 65536 || op->bd_round_max < 0 || band_ring(op).ns < 2))
             return fail(KPL_EINVAL, "bad window SpMV layout");
@@ -307,7 +307,7 @@ template <> struct band_capable<InVec<KPL_PC_IDENTITY, 0>> : std::true_type {};
 template <class SIn>
 bool band_ok(const kpl_op *op, const SIn &in) {
     if constexpr (band_capable<SIn>::value) {
-        return op->bd_val && op->chunks_global <= 0 && !((reinterpret_cast<uintptr_t>(in.a0) | reinterpret_cast<uintptr_t>(in.a1)) & 15);
+        return op->bd_stream && op->chunks_global <= 0 && !((reinterpret_cast<uintptr_t>(in.a0) | reinterpret_cast<uintptr_t>(in.a1)) & 15);
     } else {
         return false;
     }
@@ -317,8 +317,8 @@ template <class SIn>
 void launch_band(const kpl_op *op, const SIn &in, double *out, const Ws &ws, int pred, long long row,
                  cudaStream_t st) {
     if constexpr (band_capable<SIn>::value) {
-        const BandGeo bg{op->bd_val, op->bd_col, op->bd_row, op->bd_len, op->bd_grp,
-                         reinterpret_cast<const int4 *>(op->bd_sb), op->bd_win, op->bd_w, op->bd_rows};
+        const BandGeo bg{op->bd_stream, op->bd_roff, reinterpret_cast<const int4 *>(op->bd_sb), op->bd_win,
+                         op->bd_w, op->bd_rows};
         const BandRing ring = band_ring(op);
         auto kern = csr_band_ring_spmv<SIn>;
         const size_t smem = ring.bytes(op->bd_rows, op->bd_w);

@@ -30,29 +30,31 @@
 // run out of L1 miss slots long before the DRAM rate (measured on the first
 // form of this kernel: 17 of 32 warps on the long scoreboard, DRAM at 40 %).  A
 // producer warp moves the stream with cp.async.bulk into a ring of shared-memory
-// slots, one slot per "round" (32 groups: their entries, slot rows, slot lengths
-// and group offsets -- five contiguous slices of the bd_* arrays):
+// slots, one slot per "round" (32 groups).  A bulk copy occupies the SM's copy
+// engine for ~0.3 us whatever its size (tools/bulk_stream_bench.cu: 8 KB copies
+// stream at 21 GB/s per SM, 24 KB ones at 47), so a round is ONE record of the
+// byte stream bd_stream -- group offsets, slot lengths, slot rows, columns, values
+// -- and one copy; with five slices per round the stream was capped at 3 TB/s.
 //
 //   smem = | sums[rows] | window 0 [W] | window 1 [W] | ring[ns] | barriers |
-//   slot = | val[cap] | col[cap] | row[1024] | len[1024] | grp[36] |     cap % 64 == 0
+//   slot = record = | grp[36] pad | len[1024] | row[1024] | col[cnt] | val[cnt] |   cnt <= cap
 //   barriers: xfull[2] (input windows), full[ns] (1 arrival + bytes), empty[ns] (16 arrivals)
 //
 //   warp 16 (producer)                           warps 0..15 (consumers)
 //   ------------------------------------        ---------------------------------------------------------
 //   round boundaries 32 at a time (one per       per pass: wait the window; per round: wait full[slot],
 //   lane); per round: wait empty[slot],          walk groups w and w + 16 (two independent chains),
-//   expect_tx, 5 bulk copies                     arrive on empty[slot]; bar.sync among consumers, window j+2
+//   expect_tx, 1 bulk copy                       arrive on empty[slot]; bar.sync among consumers, window j+2
 #pragma once
 #include "kpl_spmv_tma.cuh"
 
 namespace kpl {
 
+constexpr int BAND_HEAD = 160 + 1024 + 2048;       // record bytes before the entries
+
 struct BandGeo {
-    const double *val;
-    const unsigned short *col;
-    const unsigned short *rowi;
-    const unsigned char *len;
-    const int *grp;
+    const unsigned char *stream;  // round records
+    const int *roff;              // record r = bytes 16 roff[r] .. 16 roff[r+1]
     const int4 *sb;           // {first pass, passes, -, -}
     const int *win;           // first column of every pass (even)
     int W, rows;
@@ -60,7 +62,7 @@ struct BandGeo {
 
 struct BandRing {
     int cap, ns;
-    __host__ __device__ size_t slot() const { return 10 * (size_t)cap + 3 * 1024 + 144; }
+    __host__ __device__ size_t slot() const { return 10 * (size_t)cap + BAND_HEAD; }
     __host__ __device__ size_t bytes(int rows, int W) const {
         return 8 * (size_t)rows + 16 * (size_t)W + ns * slot() + 8 * (2 + 2 * (size_t)ns);
     }
@@ -116,28 +118,20 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
     if (warp == BAND_CW) {
         // ------------------------------------------------------------ producer
         const int nq = npass * RP;                     // rounds of this super-block
-        const long long g0 = (long long)pass0 * RP * 32;   // its first group
+        const long long r0 = (long long)pass0 * RP;    // its first round
         int s = 0, wrap = 0;
         for (int qb = 0; qb < nq; qb += 32) {
-            // round boundaries of the next 32 rounds, one per lane
+            // record bounds of the next 32 rounds, one per lane
             const int q = min(qb + lane, nq - 1);
-            const int eb = __ldg(B.grp + g0 + 32LL * q), ee = __ldg(B.grp + g0 + 32LL * q + 32);
+            const int ob = __ldg(B.roff + r0 + q), oe = __ldg(B.roff + r0 + q + 1);
             const int m = min(32, nq - qb);
             for (int l = 0; l < m; ++l) {
-                const int e0 = __shfl_sync(0xffffffffu, eb, l), e1 = __shfl_sync(0xffffffffu, ee, l);
+                const int o0 = __shfl_sync(0xffffffffu, ob, l), o1 = __shfl_sync(0xffffffffu, oe, l);
                 if (lane == 0) {
                     if (wrap) mbar_wait_sleep(&empty[s], (unsigned)((wrap - 1) & 1));
-                    unsigned char *slot = ring + s * SLOT;
-                    const unsigned cnt = (unsigned)(e1 - e0);      // a multiple of 32 entries
-                    const long long gq = g0 + 32LL * (qb + l);
-                    mbar_expect_tx(&full[s], cnt * 10u + 3u * 1024u + 144u);
-                    if (cnt) {
-                        bulk_g2s(slot, B.val + e0, cnt * 8u, &full[s]);
-                        bulk_g2s(slot + 8 * (size_t)R.cap, B.col + e0, cnt * 2u, &full[s]);
-                    }
-                    bulk_g2s(slot + 10 * (size_t)R.cap, B.rowi + gq * 32, 2048u, &full[s]);
-                    bulk_g2s(slot + 10 * (size_t)R.cap + 2048, B.len + gq * 32, 1024u, &full[s]);
-                    bulk_g2s(slot + 10 * (size_t)R.cap + 3072, B.grp + gq, 144u, &full[s]);
+                    const unsigned bytes = (unsigned)(o1 - o0) * 16u;
+                    mbar_expect_tx(&full[s], bytes);
+                    bulk_g2s(ring + s * SLOT, B.stream + 16LL * o0, bytes, &full[s]);
                 }
                 if (++s == R.ns) { s = 0; ++wrap; }
             }
@@ -155,9 +149,9 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
         if (len & 1) dst[len - 1] = x[w0 + len - 1];
         const unsigned bytes = (unsigned)((len & ~1LL) * 8);
         mbar_expect_tx(&xfull[j & 1], bytes);
-        for (unsigned o = 0; o < bytes; o += 32768u)
+        for (unsigned o = 0; o < bytes; o += 65536u)          // few, large copies (see above)
             bulk_g2s(reinterpret_cast<unsigned char *>(dst) + o, reinterpret_cast<const unsigned char *>(x + w0) + o,
-                     min(32768u, bytes - o), &xfull[j & 1]);
+                     min(65536u, bytes - o), &xfull[j & 1]);
     };
     if (tid == 0) {
         issue(0);
@@ -171,12 +165,12 @@ csr_band_ring_spmv(long long n, BandGeo B, BandRing R, In in, double *__restrict
         for (int i = 0; i < RP; ++i) {
             mbar_wait_sleep(&full[s], ph);
             const unsigned char *slot = ring + s * SLOT;
-            const double *sval = reinterpret_cast<const double *>(slot);
-            const unsigned short *scol = reinterpret_cast<const unsigned short *>(slot + 8 * (size_t)R.cap);
-            const unsigned short *srow = reinterpret_cast<const unsigned short *>(slot + 10 * (size_t)R.cap);
-            const unsigned char *slen = slot + 10 * (size_t)R.cap + 2048;
-            const int *sgrp = reinterpret_cast<const int *>(slot + 10 * (size_t)R.cap + 3072);
+            const int *sgrp = reinterpret_cast<const int *>(slot);
+            const unsigned char *slen = slot + 160;
+            const unsigned short *srow = reinterpret_cast<const unsigned short *>(slot + 160 + 1024);
+            const unsigned short *scol = reinterpret_cast<const unsigned short *>(slot + BAND_HEAD);
             const int e0 = sgrp[0];
+            const double *sval = reinterpret_cast<const double *>(slot + BAND_HEAD + 2 * (size_t)(sgrp[32] - e0));
             // groups w and w + 16 of the round: two independent chains, interleaved.  Lane 0 holds
             // the group's longest row, lane 31 its shortest.
             const unsigned la = slen[tid], lb = slen[NC + tid];

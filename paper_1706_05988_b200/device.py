@@ -142,6 +142,7 @@ _BAND_MIN_ROW_NNZ = 16.0             # ... on rows longer than 16 nonzeros on av
 _BAND_MAX_DESC_BYTES = 0.35          # the 3 B per (row, pass) descriptors stay under 35 % of the 10 B/nnz stream
 _BAND_ROWS_MAX = 4608                # super-block height: 36 KiB of running sums at most
 _BAND_WINDOWS = (8192, 7168, 6144, 5120, 4096, 3072, 2048)
+_BAND_REC_HEAD = 160 + 1024 + 2048   # bytes of a round record before its entries: grp[36] + pad, len[1024], row[1024]
 _SMS = 148
 
 
@@ -162,11 +163,11 @@ def band_ring_slots(rows, W, round_max):
     (kpl_capi.cu:band_ring computes the same)."""
     cap = (round_max + 63) // 64 * 64
     room = _BAND_SMEM - 8 * rows - 16 * W - 128
-    return max(0, min(12, room // (10 * cap + 3 * 1024 + 144)))
+    return max(0, min(12, room // (10 * cap + _BAND_REC_HEAD)))
 
 
 def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, window=None, rows=None):
-    """(bd_val, bd_col, bd_row, bd_len, bd_grp, bd_sb, rows, W, round_max, bd_win) or None --
+    """(bd_stream, bd_roff, bd_sb, bd_win, rows, W, round_max) or None --
     the layout include/kpl_b200.h documents under kpl_op.bd_*.  Index work only (the
     values are permuted, never combined), done once per matrix with torch on the device
     the CSR arrays live on."""
@@ -273,15 +274,39 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
     k = idx - t.cummax(t.where(first, idx, t.zeros_like(idx)), 0)[0]
     slot = slot_of_row.view(-1)[p * RBP + lrow]
     pos = gstart[p * G + slot // 32] + k * 32 + slot % 32
-    bd_val = values.new_zeros(S + 64)
-    bd_col = t.zeros(S + 64, dtype=t.int16, device=dev)
-    bd_val[pos] = values
-    bd_col[pos] = (rel - (rel // W) * W).to(t.int32).to(t.int16)      # < 65536: uint16 bits
-    bd_grp = t.full((NP * G + 8,), S, dtype=t.int32, device=dev)      # terminal entry + bulk-copy slack
-    bd_grp[:NP * G] = gstart.to(t.int32)
+    # one record per round (32 groups), copied by ONE bulk copy: a bulk copy costs ~0.3 us of the
+    # SM's copy engine whatever its size (tools/bulk_stream_bench.cu), so five slices per round
+    # (values, columns, rows, lengths, offsets) capped the stream at 3 TB/s
+    NR = NP * RP
+    gstart_r = gstart.view(NR, 32)
+    rcnt = gsz.view(NR, 32).sum(1)                                     # entries per round
+    rbytes = _BAND_REC_HEAD + 10 * rcnt
+    roff = t.zeros(NR + 1, dtype=t.int64, device=dev)
+    roff[1:] = t.cumsum(rbytes, 0)
+    total = int(roff[-1])
+    if total // 16 >= 2**31:
+        return None
+    stream = t.zeros(total + 64, dtype=t.uint8, device=dev)
+    rbase = roff[:-1]
+    # grp[36]: the 32 group starts, the round's end, padding
+    s32 = stream.view(t.int32)
+    gi = (rbase // 4).unsqueeze(1) + t.arange(33, device=dev)
+    gv = t.cat([gstart_r, (gstart_r[:, :1] + rcnt.unsqueeze(1))], 1)
+    s32[gi.reshape(-1)] = gv.reshape(-1).to(t.int32)
+    # len[1024], row[1024]
+    sl = t.arange(1024, device=dev)
+    stream[((rbase + 160).unsqueeze(1) + sl).reshape(-1)] = bd_len.view(-1).to(t.uint8)
+    s16 = stream.view(t.int16)
+    s16[(((rbase + 160 + 1024) // 2).unsqueeze(1) + sl).reshape(-1)] = bd_row.view(-1).to(t.int32).to(t.int16)
+    # col[cnt], val[cnt]: entry e of round r sits at e - (first entry of the round)
+    rnd = (p * G + slot // 32) // 32
+    local = pos - gstart_r[:, 0][rnd]
+    s16[(rbase[rnd] + _BAND_REC_HEAD) // 2 + local] = (rel - (rel // W) * W).to(t.int32).to(t.int16)   # uint16 bits
+    s64 = stream.view(t.float64)
+    s64[(rbase[rnd] + _BAND_REC_HEAD + 2 * rcnt[rnd]) // 8 + local] = values
+    bd_roff = (roff // 16).to(t.int32)
     bd_sb = t.stack([pass0, npass, t.zeros_like(c_lo), t.zeros_like(c_lo)], 1).to(t.int32).contiguous()
-    return (bd_val, bd_col, bd_row.view(-1).to(t.int32).to(t.int16).contiguous(),
-            bd_len.view(-1).to(t.uint8).contiguous(), bd_grp, bd_sb, RB, W, round_max, win.to(t.int32).contiguous())
+    return stream, bd_roff, bd_sb, win.to(t.int32).contiguous(), RB, W, round_max
 
 
 # Column-sorted SpMV gathers (kpl_op.sp_*): meant for matrices whose CSR-order
@@ -472,10 +497,8 @@ def make_op(dm: DeviceMatrix, dp: DevicePrecond | None = None, zc=0, vx=0, chunk
             op.sp_col, op.sp_val, op.sp_dest = ptr(sc), ptr(sv), ptr(sd)
             op.sp_rows, op.sp_max = R, most
         if dm.band is not None:
-            bv, bc, br, bl, bg, bs, rows, W, round_max, bw = dm.band
-            op.bd_win = ptr(bw)
-            op.bd_val, op.bd_col, op.bd_row, op.bd_len = ptr(bv), ptr(bc), ptr(br), ptr(bl)
-            op.bd_grp, op.bd_sb = ptr(bg), ptr(bs)
+            st, ro, bs, bw, rows, W, round_max = dm.band
+            op.bd_stream, op.bd_roff, op.bd_sb, op.bd_win = ptr(st), ptr(ro), ptr(bs), ptr(bw)
             op.bd_rows, op.bd_w, op.bd_round_max = rows, W, round_max
     op.zc = zc
     op.vx = vx

@@ -11,14 +11,15 @@ from paper_1706_05988_b200 import problems
 from paper_1706_05988_b200.sparse import SparseMatrix
 
 
+HEAD = 160 + 1024 + 2048
+
+
 def walk(layout, n, x):
-    """What csr_band_ring_spmv computes, one (super-block, pass, group, lane) at a time."""
-    val, col, row, ln, grp, sb, RB, W, round_max, win = layout
-    win = win.numpy()
-    val, col, row = val.numpy(), col.numpy().view(np.uint16), row.numpy().view(np.uint16)
-    ln, grp, sb = ln.numpy(), grp.numpy(), sb.numpy()
+    """What csr_band_ring_spmv computes, one (super-block, pass, round record, group, lane) at a time."""
+    stream, roff, sb, win, RB, W, round_max = layout
+    raw = stream.numpy()
+    roff, sb, win = roff.numpy().astype(np.int64) * 16, sb.numpy(), win.numpy()
     RP = -(-RB // 1024)
-    RBP, G = 1024 * RP, 32 * RP
     out = np.zeros(n)
     seen = 0
     for s in range(sb.shape[0]):
@@ -28,19 +29,23 @@ def walk(layout, n, x):
             p = pass0 + j
             w0 = int(win[p])
             assert w0 % 2 == 0 and (j == 0 or w0 > int(win[p - 1]))         # ascending windows
-            assert int(ln[p * RBP:(p + 1) * RBP].sum()) > 0                   # no empty pass is stored
-            rows_seen = []
+            rows_seen, pass_nnz = [], 0
             for i in range(RP):
-                e0 = int(grp[p * G + 32 * i])
-                assert int(grp[p * G + 32 * i + 32]) - e0 <= round_max
-                for g in range(32 * i, 32 * i + 32):
-                    lens = ln[p * RBP + 32 * g: p * RBP + 32 * g + 32].astype(np.int64)
-                    rws = row[p * RBP + 32 * g: p * RBP + 32 * g + 32].astype(np.int64)
-                    base = int(grp[p * G + g])
+                r = p * RP + i
+                rec = raw[roff[r]:roff[r + 1]]
+                grp = rec[:144].view(np.int32)
+                cnt = int(grp[32] - grp[0])
+                assert len(rec) == HEAD + 10 * cnt and cnt <= round_max and cnt % 32 == 0
+                ln = rec[160:160 + 1024].astype(np.int64)
+                rw = rec[160 + 1024:HEAD].view(np.uint16).astype(np.int64)
+                col = rec[HEAD:HEAD + 2 * cnt].view(np.uint16)
+                val = rec[HEAD + 2 * cnt:HEAD + 10 * cnt].view(np.float64)
+                for g in range(32):
+                    lens, rws = ln[32 * g:32 * g + 32], rw[32 * g:32 * g + 32]
+                    base = int(grp[g] - grp[0])
                     L = int(lens.max(initial=0))
-                    assert L == int(lens[0]) and base % 32 == 0      # longest row first
-                    assert np.all(np.diff(lens) <= 0)
-                    assert int(grp[p * G + g + 1]) - base == 32 * L
+                    assert L == int(lens[0]) and np.all(np.diff(lens) <= 0)  # longest row first
+                    assert int(grp[g + 1] - grp[g]) == 32 * L
                     for k in range(L):
                         for lane in range(32):
                             e = base + 32 * k + lane
@@ -52,7 +57,9 @@ def walk(layout, n, x):
                             else:
                                 assert val[e] == 0.0 and col[e] == 0    # zero fill past the row's end
                     rows_seen.extend(rws[lens > 0].tolist())
+                    pass_nnz += int(lens.sum())
             assert len(rows_seen) == len(set(rows_seen))              # a row has one slot per pass
+            assert pass_nnz > 0                                       # no empty pass is stored
         r0 = s * RB
         m = min(RB, n - r0)
         out[r0:r0 + m] = acc[:m]
