@@ -21,7 +21,6 @@
 #include "kpl_tma.cuh"
 #include "kpl_ic0.cuh"
 #include "kpl_peer.cuh"
-#include "kpl_spmv_tma.cuh"
 #include "kpl_spmv_band.cuh"
 
 using namespace kpl;
@@ -52,6 +51,27 @@ long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 long long align256(long long v) { return (v + 255) & ~255LL; }
 
 constexpr int kSMs = 148;
+
+// 256-row blocks per reduction chunk when the caller leaves it open.  csr_chunk_sweep runs one CTA
+// per chunk, 3 CTAs per SM: with 8 blocks per chunk config 5 (977 chunks on 444 slots) takes three
+// waves for 2.2 waves of work.  On one GPU a chunk length in 6..12 that fills whole waves markedly
+// better (> 5 % of a wave) is taken instead; row-block partitions keep 8 (ranks must agree on the
+// chunks: pass kpl_op.chunk_blocks explicitly to match a single-GPU solve of a large matrix).
+int default_chunk_blocks(long long blocks, bool partitioned) {
+    const long long slots = 3LL * kSMs;
+    if (partitioned || cdiv(blocks, 8) <= slots) return 8;
+    auto eff = [&](int cb) {
+        const double w = (double)cdiv(blocks, cb) / (double)slots;
+        return w / std::ceil(w);
+    };
+    int best = 8;
+    double be = eff(8);
+    for (int cb : {9, 10, 7, 11, 6, 12}) {
+        const double e = eff(cb);
+        if (e > be + 0.05) { best = cb; be = e; }
+    }
+    return best;
+}
 
 // ring slots of the window SpMV that fit next to the running sums and the two windows
 // (device.py:band_ring_slots computes the same)
@@ -99,7 +119,7 @@ int make_layout(const kpl_op *op, Layout &L) {
         if (op->row_ptr && ((!op->col_idx && op->nnz) || (!op->values && op->nnz)))
             return fail(KPL_EINVAL, "CSR arrays missing");
         const long long blocks = cdiv(op->n, RB);
-        const int cb = op->chunk_blocks > 0 ? op->chunk_blocks : 8;
+        const int cb = op->chunk_blocks > 0 ? op->chunk_blocks : default_chunk_blocks(blocks, op->chunks_global > 0);
         if (cb > 64) return fail(KPL_EINVAL, "chunk_blocks must be <= 64");
         if (op->sp_col && (!op->sp_val || !op->sp_dest || op->sp_rows < 1 || op->sp_max < 1 ||
                            op->sp_max > 65535 || 8LL * op->sp_max > 227 * 1024))
@@ -270,19 +290,8 @@ void launch_sorted(const kpl_op *op, const CGeo &g, const SIn &in, double *out, 
     static const int per = [] { const char *e = std::getenv("KPL_SORTED_PER"); return e ? std::atoi(e) : 4; }();
     const SGather sg{op->sp_col, op->sp_val, reinterpret_cast<const unsigned short *>(op->sp_dest), op->sp_rows};
     const long long nblk = cdiv(op->n, op->sp_rows);
-    // idle replacement sweeps (PRED_FIRE) keep a small grid, as the other sweeps
-    // default: the bulk-TMA-fed kernel (matrix stream off the LSU queue), one CTA per SM
-    static const bool plain = [] { const char *e = std::getenv("KPL_SORTED_KERNEL"); return e && !std::strcmp(e, "plain"); }();
-    using RG = SpRing<2048, 2>;
-    const size_t tsmem = RG::bytes(op->sp_max);
-    static const int lag = [] { const char *e = std::getenv("KPL_SORTED_LAG"); return e ? std::atoi(e) : 2; }();
-    if (!plain && tsmem <= 227 * 1024) {
-        auto kern = lag == 1 ? csr_sorted_tma_spmv<SIn, 512, 2048, 2, 1> : csr_sorted_tma_spmv<SIn, 512, 2048, 2, 2>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-        const unsigned tgrid = (unsigned)std::min(nblk, (long long)kSMs);
-        launch_pdl(kern, tgrid, 512 + 32, tsmem, st, g, sg, in, out, ws, pred, row);
-        return;
-    }
+    // (a bulk-TMA-fed variant of this kernel was removed in r2: tools/stress_spmv.py found it returning
+    // wrong rows in ~2 % of the launches under concurrent load)
     const size_t smem = 8 * (size_t)op->sp_max;
     // persistent: one CTA per SM (two when the products fit twice), striding over the
     // blocks so the next block's first stream loads overlap this block's row sums

@@ -46,9 +46,18 @@
 //   lane); per round: wait empty[slot],          walk groups w and w + 16 (two independent chains),
 //   expect_tx, 1 bulk copy                       arrive on empty[slot]; bar.sync among consumers, window j+2
 #pragma once
-#include "kpl_spmv_tma.cuh"
+#include "kpl_tma.cuh"
 
 namespace kpl {
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// barrier among the consumer threads only (the producer warp does not take part)
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
 
 constexpr int BAND_HEAD = 160 + 1024 + 2048;       // record bytes before the entries
 

@@ -316,8 +316,7 @@ def band_layout(row_ptr_h, col_idx_h, row_ptr, col_idx, values, mode=None, windo
 # ms/iteration), so it is opt-in: KPL_CSR_GATHER = csr (default)
 # | sorted | auto (sorted when a CSR-order warp gather touches >= 12 lines).
 _SORTED_MIN_LINES = 12.0
-# products of one block live in shared memory next to the bulk-copy ring of
-# csr_sorted_tma_spmv (2 x 2048 nonzeros x 14 B): 227 KiB - 56 KiB -> 21,872
+# products of one block live in shared memory (8 bytes each; two CTAs per SM fit up to ~14,000)
 _SORTED_MAX_NNZ = 21_800
 
 

@@ -15,7 +15,7 @@ After each solve
 
 Every kernel family runs: TMA 3D and 2D sweeps, the register sweep, the
 persistent small-problem solver, the split CSR path (window and pipelined
-SpMV), both column-sorted SpMVs, IC(0), p-CG-rr replacement, gap
+SpMV), the window and the column-sorted SpMV, IC(0), p-CG-rr replacement, gap
 instrumentation, classic CG and the reference reduction order.
 """
 
@@ -85,8 +85,8 @@ CASES = [
      {"env": ("KPL_CSR_GATHER", "band"), "env2": ("KPL_BAND_W", "1022")}),
     ("csr_sorted", lambda: (problems.banded_spd(20_000, seed=2, band=3000), "jacobi"),
      dict(method="pcg_sh", shift=0.4), {"env": ("KPL_CSR_GATHER", "sorted")}),
-    ("csr_sorted_plain", lambda: (problems.banded_spd(20_000, seed=2, band=3000), "jacobi"),
-     dict(method="pcg", shift=0.0), {"env": ("KPL_CSR_GATHER", "sorted"), "env2": ("KPL_SORTED_KERNEL", "plain")}),
+    ("csr_sorted_pcg", lambda: (problems.banded_spd(20_000, seed=2, band=3000), "jacobi"),
+     dict(method="pcg", shift=0.0), {"env": ("KPL_CSR_GATHER", "sorted")}),
     ("ic0", lambda: (K.laplacian_2d(30, 20), "ic0"), dict(method="pcg_sh", shift=0.3), {}),
     ("gaps", lambda: (K.Stencil2D(50, 40), None), dict(method="pcg_sh", shift=1.0, track_gaps=True), {}),
     ("cg", lambda: (K.laplacian_2d(70, 50), "jacobi"), dict(method="cg"), {}),
