@@ -52,27 +52,6 @@ long long align256(long long v) { return (v + 255) & ~255LL; }
 
 constexpr int kSMs = 148;
 
-// 256-row blocks per reduction chunk when the caller leaves it open.  csr_chunk_sweep runs one CTA
-// per chunk, 3 CTAs per SM: with 8 blocks per chunk config 5 (977 chunks on 444 slots) takes three
-// waves for 2.2 waves of work.  On one GPU a chunk length in 6..12 that fills whole waves markedly
-// better (> 5 % of a wave) is taken instead; row-block partitions keep 8 (ranks must agree on the
-// chunks: pass kpl_op.chunk_blocks explicitly to match a single-GPU solve of a large matrix).
-int default_chunk_blocks(long long blocks, bool partitioned) {
-    const long long slots = 3LL * kSMs;
-    if (partitioned || cdiv(blocks, 8) <= slots) return 8;
-    auto eff = [&](int cb) {
-        const double w = (double)cdiv(blocks, cb) / (double)slots;
-        return w / std::ceil(w);
-    };
-    int best = 8;
-    double be = eff(8);
-    for (int cb : {9, 10, 7, 11, 6, 12}) {
-        const double e = eff(cb);
-        if (e > be + 0.05) { best = cb; be = e; }
-    }
-    return best;
-}
-
 // ring slots of the window SpMV that fit next to the running sums and the two windows
 // (device.py:band_ring_slots computes the same)
 BandRing band_ring(const kpl_op *op) {
@@ -119,7 +98,7 @@ int make_layout(const kpl_op *op, Layout &L) {
         if (op->row_ptr && ((!op->col_idx && op->nnz) || (!op->values && op->nnz)))
             return fail(KPL_EINVAL, "CSR arrays missing");
         const long long blocks = cdiv(op->n, RB);
-        const int cb = op->chunk_blocks > 0 ? op->chunk_blocks : default_chunk_blocks(blocks, op->chunks_global > 0);
+        const int cb = op->chunk_blocks > 0 ? op->chunk_blocks : 8;
         if (cb > 64) return fail(KPL_EINVAL, "chunk_blocks must be <= 64");
         if (op->sp_col && (!op->sp_val || !op->sp_dest || op->sp_rows < 1 || op->sp_max < 1 ||
                            op->sp_max > 65535 || 8LL * op->sp_max > 227 * 1024))
