@@ -1,6 +1,6 @@
 """Device time of N p-CG-sh iteration sweeps (no result check) -- A/B timing helper.
 
-    KPL_CSR_GATHER=csr|sorted KPL_SORTED_NT=256|512|1024 python tools/csr_iter_time.py [c2c,c4,c5] [chunk_blocks]
+    KPL_CSR_GATHER=auto|band|csr|sorted [KPL_LONG=1] python tools/csr_iter_time.py [c2c,c4,c5] [chunk_blocks]
 
 Matrices are cached under /tmp/kpl_cache (generation of config 5 takes ~30 s).
 """

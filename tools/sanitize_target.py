@@ -6,7 +6,7 @@
 
 Families: tma (TMA-fed 3D sweep), reg (register stencil sweep), persist
 (persistent small-problem solver), csr (split CSR SpMV + chunk sweep, pipelined
-SpMV), sorted (column-sorted SpMV, plain and bulk-TMA), ic0 (IC(0) factor +
+SpMV), sorted (column-sorted SpMV), band (window SpMV), ic0 (IC(0) factor +
 substitution sweeps), peer (virtual-rank peer exchange: fused sweep with the
 deferred fold, post kernels, finalize), order (reference reduction order).
 Each runs a few iterations and checks the result against a second run of the
